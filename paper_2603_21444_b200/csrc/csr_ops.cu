@@ -1,0 +1,519 @@
+// Device CSR store and the non-multiply kernels of the hot path:
+//   spgeam   (reference csr.cpp:167-196)  — partial-C merge
+//   vconcat  (reference csr.cpp:348-363)  — data effect of the node allgather
+//   extract  (reference partition.cpp:161-222, one tile)
+//   column_normalize / prune (reference csr.cpp:224-249) — MCL post-step
+//   check_canonical (reference csr.cpp:30-50)
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <climits>
+
+#include "spg_internal.cuh"
+
+namespace spgb {
+namespace {
+
+int grid_for(spg_ctx* ctx, int64_t n, int bs = 256) {
+    const int64_t want = (n + bs - 1) / bs;
+    const int64_t cap = int64_t(ctx->num_sms) * 16;
+    return static_cast<int>(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+#define GRID_STRIDE(i, n) \
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < (n); i += int64_t(gridDim.x) * blockDim.x)
+
+// ----------------------------------------------------------------- spgeam
+// Warp per row: merge-path split of the two sorted rows among the 32 lanes,
+// each lane merges its diagonal segment sequentially. Pass 1 counts the
+// union size per row; pass 2 writes at the scanned offsets.
+__device__ __forceinline__ int64_t merge_path(const int32_t* a, int64_t na, const int32_t* b, int64_t nb,
+                                              int64_t diag) {
+    // number of elements taken from `a` at diagonal `diag` (a wins ties: a[i] <= b[j] goes first)
+    int64_t lo = diag > nb ? diag - nb : 0;
+    int64_t hi = diag < na ? diag : na;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (a[mid] <= b[diag - 1 - mid]) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+template <bool WRITE>
+__global__ void k_spgeam(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
+                         const double* __restrict__ aval, const int64_t* __restrict__ brp,
+                         const int32_t* __restrict__ bcol, const double* __restrict__ bval, int64_t m,
+                         int64_t* __restrict__ cnt, const int64_t* __restrict__ crp, int32_t* __restrict__ ccol,
+                         double* __restrict__ cval) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t i = warp; i < m; i += nwarps) {
+        const int64_t a0 = arp[i], na = arp[i + 1] - a0;
+        const int64_t b0 = brp[i], nb = brp[i + 1] - b0;
+        const int32_t* ac = acol + a0;
+        const int32_t* bc = bcol + b0;
+        const int64_t tot = na + nb;
+        const int64_t per = (tot + 31) / 32;
+        const int64_t d0 = ::min(tot, per * lane), d1 = ::min(tot, per * (lane + 1));
+        int64_t ia = merge_path(ac, na, bc, nb, d0);
+        int64_t ib = d0 - ia;
+        const int64_t ia_end = merge_path(ac, na, bc, nb, d1);
+        const int64_t ib_end = d1 - ia_end;
+        // An equal pair (a[ia]==b[ib]) is merged into one output by the lane that
+        // consumes the `a` element; a lane whose first element is a `b` equal to
+        // the preceding `a` skips it.
+        int64_t out = 0;
+        int64_t o = WRITE ? crp[i] : 0;
+        int64_t wpos = 0;
+        if (WRITE) {
+            // exclusive prefix of per-lane counts computed in a first sweep
+            int64_t c = 0;
+            {
+                int64_t xa = ia, xb = ib;
+                while (xa < ia_end || xb < ib_end) {
+                    const int32_t ja = xa < na ? ac[xa] : INT_MAX;
+                    const int32_t jb = xb < nb ? bc[xb] : INT_MAX;
+                    if (xa < ia_end && (xb >= ib_end || ja <= jb)) {
+                        ++c;
+                        if (xb < nb && ja == jb) ++xb;  // merged pair (may extend past ib_end)
+                        ++xa;
+                    } else {
+                        // a `b` element: skip if it equals the previous `a` (consumed by earlier lane)
+                        if (!(xa > 0 && ac[xa - 1] == jb)) ++c;
+                        ++xb;
+                    }
+                }
+            }
+            int64_t inc = c;
+#pragma unroll
+            for (int s = 1; s < 32; s <<= 1) {
+                const int64_t y = __shfl_up_sync(0xffffffffu, inc, s);
+                if (lane >= s) inc += y;
+            }
+            wpos = o + inc - c;
+        }
+        int64_t xa = ia, xb = ib;
+        while (xa < ia_end || xb < ib_end) {
+            const int32_t ja = xa < na ? ac[xa] : INT_MAX;
+            const int32_t jb = xb < nb ? bc[xb] : INT_MAX;
+            if (xa < ia_end && (xb >= ib_end || ja <= jb)) {
+                if (xb < nb && ja == jb) {
+                    if (WRITE) {
+                        ccol[wpos] = ja;
+                        cval[wpos] = __dadd_rn(aval[a0 + xa], bval[b0 + xb]);
+                    }
+                    ++xb;
+                } else if (WRITE) {
+                    ccol[wpos] = ja;
+                    cval[wpos] = aval[a0 + xa];
+                }
+                ++out;
+                ++wpos;
+                ++xa;
+            } else {
+                if (!(xa > 0 && ac[xa - 1] == jb)) {
+                    if (WRITE) {
+                        ccol[wpos] = jb;
+                        cval[wpos] = bval[b0 + xb];
+                    }
+                    ++out;
+                    ++wpos;
+                }
+                ++xb;
+            }
+        }
+        if (!WRITE) {
+            int64_t s = out;
+#pragma unroll
+            for (int k = 16; k > 0; k >>= 1) s += __shfl_xor_sync(0xffffffffu, s, k);
+            if (lane == 0) cnt[i] = s;
+        }
+    }
+}
+
+// ----------------------------------------------------------------- vconcat
+__global__ void k_rebase_rowptr(const int64_t* __restrict__ src, int64_t rows, int64_t base,
+                                int64_t* __restrict__ dst) {
+    GRID_STRIDE(i, rows) dst[i] = base + src[i + 1];
+}
+
+// ----------------------------------------------------------------- extract
+__device__ __forceinline__ int64_t lower_bound_i32(const int32_t* p, int64_t lo, int64_t hi, int64_t v) {
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (p[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_extract_count(const int64_t* __restrict__ rp, const int32_t* __restrict__ col, int64_t r0,
+                                int64_t rows, int64_t c0, int64_t c1, int64_t* __restrict__ beg,
+                                int64_t* __restrict__ cnt) {
+    GRID_STRIDE(i, rows) {
+        const int64_t lo = rp[r0 + i], hi = rp[r0 + i + 1];
+        const int64_t a = lower_bound_i32(col, lo, hi, c0);
+        const int64_t b = lower_bound_i32(col, a, hi, c1);
+        beg[i] = a;
+        cnt[i] = b - a;
+    }
+}
+
+__global__ void k_extract_copy(const int64_t* __restrict__ beg, const int64_t* __restrict__ orp, int64_t rows,
+                               const int32_t* __restrict__ col, const double* __restrict__ val, int64_t c0,
+                               int32_t* __restrict__ ocol, double* __restrict__ oval) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t i = warp; i < rows; i += nwarps) {
+        const int64_t s = beg[i], o = orp[i], n = orp[i + 1] - o;
+        for (int64_t t = lane; t < n; t += 32) {
+            ocol[o + t] = static_cast<int32_t>(col[s + t] - c0);
+            oval[o + t] = val[s + t];
+        }
+    }
+}
+
+// ------------------------------------------------------- column_normalize
+// Column sums in CSR storage order (reference csr.cpp:225-227): entries are
+// stably radix-sorted by column (storage index as payload), then each column is
+// summed sequentially in storage order, so sums are bit-identical.
+__global__ void k_iota_i64(int64_t* p, int64_t n) { GRID_STRIDE(i, n) p[i] = i; }
+
+__global__ void k_colsum_sorted(const int32_t* __restrict__ keys, const int64_t* __restrict__ idx, int64_t nnz,
+                                const double* __restrict__ val, double* __restrict__ colsum) {
+    // one thread per run start
+    GRID_STRIDE(t, nnz) {
+        if (t > 0 && keys[t - 1] == keys[t]) continue;
+        const int32_t c = keys[t];
+        double s = 0.0;
+        for (int64_t u = t; u < nnz && keys[u] == c; ++u) s = __dadd_rn(s, val[idx[u]]);
+        colsum[c] = s;
+    }
+}
+
+__global__ void k_scale_cols(const int32_t* __restrict__ col, double* __restrict__ val, int64_t nnz,
+                             const double* __restrict__ colsum) {
+    GRID_STRIDE(t, nnz) {
+        const double s = colsum[col[t]];
+        if (s != 0.0) val[t] = __ddiv_rn(val[t], s);
+    }
+}
+
+// -------------------------------------------------------------------- prune
+__global__ void k_prune_count(const int64_t* __restrict__ rp, const double* __restrict__ val, int64_t m,
+                              double th, int64_t* __restrict__ cnt) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t i = warp; i < m; i += nwarps) {
+        int64_t c = 0;
+        for (int64_t t = rp[i] + lane; t < rp[i + 1]; t += 32) c += !(val[t] < th);
+#pragma unroll
+        for (int k = 16; k > 0; k >>= 1) c += __shfl_xor_sync(0xffffffffu, c, k);
+        if (lane == 0) cnt[i] = c;
+    }
+}
+
+__global__ void k_prune_copy(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                             const double* __restrict__ val, int64_t m, double th, const int64_t* __restrict__ orp,
+                             int32_t* __restrict__ ocol, double* __restrict__ oval) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t i = warp; i < m; i += nwarps) {
+        int64_t o = orp[i];
+        for (int64_t base = rp[i]; base < rp[i + 1]; base += 32) {
+            const int64_t t = base + lane;
+            const bool keep = t < rp[i + 1] && !(val[t] < th);
+            const unsigned mask = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const int64_t w = o + __popc(mask & ((1u << lane) - 1));
+                ocol[w] = col[t];
+                oval[w] = val[t];
+            }
+            o += __popc(mask);
+        }
+    }
+}
+
+// -------------------------------------------------------- canonical check
+// err[0] = first offending row (or INT64_MAX), err[1] = violation code.
+__global__ void k_check(const int64_t* __restrict__ rp, const int32_t* __restrict__ col, int64_t m, int64_t ncols,
+                        int64_t nnz, unsigned long long* __restrict__ err) {
+    GRID_STRIDE(i, m) {
+        const int64_t lo = rp[i], hi = rp[i + 1];
+        int code = 0;
+        if (lo > hi) code = 1;
+        else if (hi > nnz || lo < 0) code = 2;
+        else
+            for (int64_t t = lo; t < hi; ++t) {
+                if (col[t] < 0 || col[t] >= ncols) { code = 3; break; }
+                if (t > lo && col[t - 1] >= col[t]) { code = 4; break; }
+            }
+        if (code) atomicMin(err, (static_cast<unsigned long long>(i) << 3) | code);
+    }
+}
+
+// ---------------------------------------------------------- index widening
+__global__ void k_narrow(const int64_t* __restrict__ in, int32_t* __restrict__ out, int64_t n,
+                         unsigned long long* __restrict__ bad) {
+    GRID_STRIDE(i, n) {
+        const int64_t v = in[i];
+        if (v < INT_MIN || v > INT_MAX) atomicOr(bad, 1ull);
+        out[i] = static_cast<int32_t>(v);
+    }
+}
+
+__global__ void k_widen(const int32_t* __restrict__ in, int64_t* __restrict__ out, int64_t n) {
+    GRID_STRIDE(i, n) out[i] = in[i];
+}
+
+}  // namespace
+
+// ===================================================================== host
+spg_csr* new_csr(spg_ctx* ctx, int64_t nrows, int64_t ncols, int64_t nnz) {
+    auto* m = new spg_csr;
+    m->ctx = ctx;
+    m->nrows = nrows;
+    m->ncols = ncols;
+    m->rowptr = dalloc<int64_t>(ctx, nrows + 1);
+    if (nnz >= 0) {
+        m->nnz = nnz;
+        m->colind = dalloc<int32_t>(ctx, nnz);
+        m->values = dalloc<double>(ctx, nnz);
+        if (nnz == 0) SPG_CUDA(cudaMemsetAsync(m->rowptr, 0, (nrows + 1) * sizeof(int64_t), ctx->stream));
+    }
+    return m;
+}
+
+void free_csr(spg_csr* m) {
+    if (!m) return;
+    DeviceScope ds(m->ctx->device);
+    if (m->storage == 0) {
+        dfree(m->ctx, m->rowptr);
+        dfree(m->ctx, m->colind);
+        dfree(m->ctx, m->values);
+    } else if (m->storage == 1) {
+        cudaStreamSynchronize(m->ctx->stream);
+        cudaFree(m->rowptr);
+        cudaFree(m->colind);
+        cudaFree(m->values);
+    } else {
+        cudaIpcCloseMemHandle(m->rowptr);
+        if (m->colind) cudaIpcCloseMemHandle(m->colind);
+        if (m->values) cudaIpcCloseMemHandle(m->values);
+    }
+    delete m;
+}
+
+int64_t read_scalar(spg_ctx* ctx, const int64_t* dptr) {
+    SPG_CUDA(cudaMemcpyAsync(ctx->host_scalars, dptr, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return ctx->host_scalars[0];
+}
+
+spg_csr* spgeam(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
+    if (a->nrows != b->nrows || a->ncols != b->ncols) fail(SPG_DIMENSION_ERROR, "spgeam: shape mismatch");
+    const int64_t m = a->nrows;
+    if (a->nnz == 0) return copy_csr(ctx, b);
+    if (b->nnz == 0) return copy_csr(ctx, a);
+    DBuf<int64_t> cnt(ctx, m + 1);
+    spg_csr* c = new_csr(ctx, m, a->ncols, -1);
+    const int g = grid_for(ctx, m * 32);
+    {
+        KTime kt(ctx, "spgeam_count");
+        k_spgeam<false><<<g, 256, 0, ctx->stream>>>(a->rowptr, a->colind, a->values, b->rowptr, b->colind, b->values,
+                                                     m, cnt, nullptr, nullptr, nullptr);
+        SPG_LAUNCH_CHECK();
+    }
+    exclusive_scan_i64(ctx, cnt, c->rowptr, m);
+    c->nnz = read_scalar(ctx, c->rowptr + m);
+    c->colind = dalloc<int32_t>(ctx, c->nnz);
+    c->values = dalloc<double>(ctx, c->nnz);
+    {
+        KTime kt(ctx, "spgeam_write");
+        k_spgeam<true><<<g, 256, 0, ctx->stream>>>(a->rowptr, a->colind, a->values, b->rowptr, b->colind, b->values,
+                                                    m, nullptr, c->rowptr, c->colind, c->values);
+        SPG_LAUNCH_CHECK();
+    }
+    return c;
+}
+
+spg_csr* copy_csr(spg_ctx* ctx, const spg_csr* s) {
+    spg_csr* c = new_csr(ctx, s->nrows, s->ncols, s->nnz);
+    const int sd = s->ctx->device, dd = ctx->device;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+        if (!bytes) return;
+        if (sd == dd) SPG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+        else SPG_CUDA(cudaMemcpyPeerAsync(dst, dd, src, sd, bytes, ctx->stream));
+    };
+    cp(c->rowptr, s->rowptr, (s->nrows + 1) * sizeof(int64_t));
+    cp(c->colind, s->colind, s->nnz * sizeof(int32_t));
+    cp(c->values, s->values, s->nnz * sizeof(double));
+    return c;
+}
+
+spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n) {
+    if (n == 0) return new_csr(ctx, 0, 0, 0);
+    int64_t rows = 0, nnz = 0;
+    const int64_t ncols = slices[0]->ncols;
+    for (int s = 0; s < n; ++s) {
+        if (slices[s]->ncols != ncols) fail(SPG_DIMENSION_ERROR, "vconcat: column count mismatch");
+        rows += slices[s]->nrows;
+        nnz += slices[s]->nnz;
+    }
+    spg_csr* out = new_csr(ctx, rows, ncols, nnz);
+    SPG_CUDA(cudaMemsetAsync(out->rowptr, 0, sizeof(int64_t), ctx->stream));
+    int64_t r = 0, base = 0;
+    const int dd = ctx->device;
+    for (int s = 0; s < n; ++s) {
+        const spg_csr* sl = slices[s];
+        const int sd = sl->ctx->device;
+        const int64_t* rp = sl->rowptr;
+        DBuf<int64_t> tmp(ctx, sd == dd ? 0 : sl->nrows + 1);
+        if (sd != dd) {
+            SPG_CUDA(cudaMemcpyPeerAsync(tmp.get(), dd, sl->rowptr, sd, (sl->nrows + 1) * sizeof(int64_t), ctx->stream));
+            rp = tmp.get();
+        }
+        if (sl->nrows) {
+            KTime kt(ctx, "vconcat_rebase");
+            k_rebase_rowptr<<<grid_for(ctx, sl->nrows), 256, 0, ctx->stream>>>(rp, sl->nrows, base, out->rowptr + r + 1);
+            SPG_LAUNCH_CHECK();
+        }
+        if (sl->nnz) {
+            if (sd == dd) {
+                SPG_CUDA(cudaMemcpyAsync(out->colind + base, sl->colind, sl->nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+                SPG_CUDA(cudaMemcpyAsync(out->values + base, sl->values, sl->nnz * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+            } else {
+                SPG_CUDA(cudaMemcpyPeerAsync(out->colind + base, dd, sl->colind, sd, sl->nnz * sizeof(int32_t), ctx->stream));
+                SPG_CUDA(cudaMemcpyPeerAsync(out->values + base, dd, sl->values, sd, sl->nnz * sizeof(double), ctx->stream));
+            }
+        }
+        r += sl->nrows;
+        base += sl->nnz;
+    }
+    return out;
+}
+
+spg_csr* extract(spg_ctx* ctx, const spg_csr* m, int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
+    if (r0 < 0 || r1 < r0 || r1 > m->nrows || c0 < 0 || c1 < c0 || c1 > m->ncols)
+        fail(SPG_PARAMETER_ERROR, "extract: rectangle outside the matrix");
+    const int64_t rows = r1 - r0;
+    spg_csr* t = new_csr(ctx, rows, c1 - c0, -1);
+    if (rows == 0 || m->nnz == 0) {
+        t->nnz = 0;
+        t->colind = dalloc<int32_t>(ctx, 0);
+        t->values = dalloc<double>(ctx, 0);
+        SPG_CUDA(cudaMemsetAsync(t->rowptr, 0, (rows + 1) * sizeof(int64_t), ctx->stream));
+        return t;
+    }
+    DBuf<int64_t> beg(ctx, rows), cnt(ctx, rows);
+    KTime kt(ctx, "extract");
+    k_extract_count<<<grid_for(ctx, rows), 256, 0, ctx->stream>>>(m->rowptr, m->colind, r0, rows, c0, c1, beg, cnt);
+    SPG_LAUNCH_CHECK();
+    exclusive_scan_i64(ctx, cnt, t->rowptr, rows);
+    t->nnz = read_scalar(ctx, t->rowptr + rows);
+    t->colind = dalloc<int32_t>(ctx, t->nnz);
+    t->values = dalloc<double>(ctx, t->nnz);
+    k_extract_copy<<<grid_for(ctx, rows * 32), 256, 0, ctx->stream>>>(beg, t->rowptr, rows, m->colind, m->values, c0,
+                                                                      t->colind, t->values);
+    SPG_LAUNCH_CHECK();
+    return t;
+}
+
+void column_normalize(spg_ctx* ctx, spg_csr* m) {
+    const int64_t nnz = m->nnz;
+    if (nnz == 0) return;
+    if (nnz > INT32_MAX) fail(SPG_PARAMETER_ERROR, "column_normalize: nnz exceeds 2^31");
+    DBuf<int32_t> keys(ctx, nnz);
+    DBuf<int64_t> idx(ctx, nnz), idx_sorted(ctx, nnz);
+    DBuf<double> colsum(ctx, m->ncols);
+    KTime kt(ctx, "column_normalize");
+    k_iota_i64<<<grid_for(ctx, nnz), 256, 0, ctx->stream>>>(idx, nnz);
+    int bits = 1;
+    while ((int64_t(1) << bits) < m->ncols) ++bits;
+    size_t tmp = 0;
+    SPG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, m->colind, keys.get(), idx.get(), idx_sorted.get(),
+                                             static_cast<int>(nnz), 0, bits, ctx->stream));
+    DBuf<unsigned char> t(ctx, tmp);
+    SPG_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, m->colind, keys.get(), idx.get(), idx_sorted.get(),
+                                             static_cast<int>(nnz), 0, bits, ctx->stream));
+    SPG_CUDA(cudaMemsetAsync(colsum.get(), 0, m->ncols * sizeof(double), ctx->stream));
+    k_colsum_sorted<<<grid_for(ctx, nnz), 256, 0, ctx->stream>>>(keys, idx_sorted, nnz, m->values, colsum);
+    k_scale_cols<<<grid_for(ctx, nnz), 256, 0, ctx->stream>>>(m->colind, m->values, nnz, colsum);
+    SPG_LAUNCH_CHECK();
+}
+
+spg_csr* prune(spg_ctx* ctx, const spg_csr* a, double th) {
+    if (th < 0.0) fail(SPG_PARAMETER_ERROR, "prune: negative threshold");
+    const int64_t m = a->nrows;
+    DBuf<int64_t> cnt(ctx, m + 1);
+    spg_csr* r = new_csr(ctx, m, a->ncols, -1);
+    KTime kt(ctx, "prune");
+    if (m) {
+        k_prune_count<<<grid_for(ctx, m * 32), 256, 0, ctx->stream>>>(a->rowptr, a->values, m, th, cnt);
+        SPG_LAUNCH_CHECK();
+    }
+    exclusive_scan_i64(ctx, cnt, r->rowptr, m);
+    r->nnz = read_scalar(ctx, r->rowptr + m);
+    r->colind = dalloc<int32_t>(ctx, r->nnz);
+    r->values = dalloc<double>(ctx, r->nnz);
+    if (m) {
+        k_prune_copy<<<grid_for(ctx, m * 32), 256, 0, ctx->stream>>>(a->rowptr, a->colind, a->values, m, th, r->rowptr,
+                                                                     r->colind, r->values);
+        SPG_LAUNCH_CHECK();
+    }
+    return r;
+}
+
+void check_canonical(spg_ctx* ctx, const spg_csr* m) {
+    if (m->nrows < 0 || m->ncols < 0) fail(SPG_ERROR, "negative dimension");
+    int64_t h[2];
+    SPG_CUDA(cudaMemcpyAsync(&h[0], m->rowptr, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    SPG_CUDA(cudaMemcpyAsync(&h[1], m->rowptr + m->nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (h[0] != 0) fail(SPG_ERROR, "rowptr[0] != 0");
+    if (h[1] != m->nnz) fail(SPG_ERROR, "rowptr[nrows] != nnz");
+    DBuf<unsigned long long> err(ctx, 1);
+    const unsigned long long none = ~0ull;
+    SPG_CUDA(cudaMemcpyAsync(err.get(), &none, sizeof(none), cudaMemcpyHostToDevice, ctx->stream));
+    if (m->nrows) {
+        k_check<<<grid_for(ctx, m->nrows), 256, 0, ctx->stream>>>(m->rowptr, m->colind, m->nrows, m->ncols, m->nnz, err);
+        SPG_LAUNCH_CHECK();
+    }
+    unsigned long long e = 0;
+    SPG_CUDA(cudaMemcpyAsync(&e, err.get(), sizeof(e), cudaMemcpyDeviceToHost, ctx->stream));
+    SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (e != none) {
+        const int64_t row = static_cast<int64_t>(e >> 3);
+        const int code = static_cast<int>(e & 7);
+        const char* what = code == 1 ? "rowptr not non-decreasing at row "
+                           : code == 2 ? "rowptr out of range at row "
+                           : code == 3 ? "column index out of range in row "
+                                       : "columns not strictly increasing in row ";
+        fail(SPG_ERROR, what + std::to_string(row));
+    }
+}
+
+void narrow_index(spg_ctx* ctx, const int64_t* d_in, int32_t* d_out, int64_t n) {
+    if (n == 0) return;
+    DBuf<unsigned long long> bad(ctx, 1);
+    SPG_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(unsigned long long), ctx->stream));
+    k_narrow<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(d_in, d_out, n, bad);
+    SPG_LAUNCH_CHECK();
+    unsigned long long h = 0;
+    SPG_CUDA(cudaMemcpyAsync(&h, bad.get(), sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (h) fail(SPG_PARAMETER_ERROR, "column index does not fit in 32 bits");
+}
+
+void widen_index(spg_ctx* ctx, const int32_t* d_in, int64_t* d_out, int64_t n) {
+    if (n == 0) return;
+    k_widen<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(d_in, d_out, n);
+    SPG_LAUNCH_CHECK();
+}
+
+}  // namespace spgb

@@ -1,0 +1,162 @@
+// Internal definitions shared by the CUDA translation units of libspgb200.so.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "spg/capi.h"
+
+namespace spgb {
+
+struct StatusError : std::runtime_error {
+    spg_status code;
+    StatusError(spg_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(spg_status c, const std::string& m) { throw StatusError(c, m); }
+
+#define SPG_CUDA(call)                                                                              \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess)                                                                      \
+            ::spgb::fail(e_ == cudaErrorMemoryAllocation ? SPG_OOM : SPG_CUDA_ERROR,                \
+                         std::string(#call) + " failed: " + cudaGetErrorString(e_) + " (" __FILE__ \
+                         ":" + std::to_string(__LINE__) + ")");                                     \
+    } while (0)
+
+#define SPG_LAUNCH_CHECK() SPG_CUDA(cudaGetLastError())
+
+// Per-kernel CUDA-event timing on the context stream.
+struct Timer {
+    struct Rec {
+        std::string name;
+        cudaEvent_t start, stop;
+    };
+    bool on = false;
+    std::vector<Rec> pending;
+    std::vector<cudaEvent_t> pool;
+    std::map<std::string, std::pair<int64_t, double>> totals;
+
+    cudaEvent_t ev() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        SPG_CUDA(cudaEventCreate(&e));
+        return e;
+    }
+};
+
+}  // namespace spgb
+
+struct spg_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaMemPool_t pool = nullptr;
+    int num_sms = 148;
+    size_t l2_bytes = 0;
+    spgb::Timer timer;
+    // Pinned host staging for small scalar read-backs.
+    int64_t* host_scalars = nullptr;
+    bool tile_attr_set = false;
+};
+
+struct spg_csr {
+    spg_ctx* ctx = nullptr;  // owning context (device + pool)
+    int64_t nrows = 0, ncols = 0, nnz = 0;
+    int64_t* rowptr = nullptr;  // nrows+1
+    int32_t* colind = nullptr;  // nnz
+    double* values = nullptr;   // nnz
+    // Storage kind: 0 = stream-ordered pool (default), 1 = cudaMalloc (IPC
+    // exportable), 2 = IPC view of a peer process's matrix (read-only).
+    int storage = 0;
+};
+
+namespace spgb {
+
+// RAII scope that binds the context's device.
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int dev) {
+        SPG_CUDA(cudaGetDevice(&prev));
+        if (prev != dev) SPG_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceScope() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+template <class T>
+T* dalloc(spg_ctx* ctx, size_t n) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    SPG_CUDA(cudaMallocFromPoolAsync(&p, n * sizeof(T), ctx->pool, ctx->stream));
+    return static_cast<T*>(p);
+}
+
+inline void dfree(spg_ctx* ctx, void* p) {
+    if (p) cudaFreeAsync(p, ctx->stream);
+}
+
+// Stream-ordered scratch buffer freed at scope exit.
+template <class T>
+struct DBuf {
+    spg_ctx* ctx;
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf(spg_ctx* c, size_t count) : ctx(c), n(count) { p = dalloc<T>(c, count); }
+    ~DBuf() { dfree(ctx, p); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    T* get() const { return p; }
+    operator T*() const { return p; }
+};
+
+// Kernel timing bracket: records events around a launch when timing is enabled.
+struct KTime {
+    spg_ctx* ctx;
+    const char* name;
+    cudaEvent_t s = nullptr, e = nullptr;
+    KTime(spg_ctx* c, const char* n) : ctx(c), name(n) {
+        if (ctx->timer.on) {
+            s = ctx->timer.ev();
+            e = ctx->timer.ev();
+            cudaEventRecord(s, ctx->stream);
+        }
+    }
+    ~KTime() {
+        if (s) {
+            cudaEventRecord(e, ctx->stream);
+            ctx->timer.pending.push_back({name, s, e});
+        }
+    }
+};
+
+spg_csr* new_csr(spg_ctx* ctx, int64_t nrows, int64_t ncols, int64_t nnz);
+void free_csr(spg_csr* m);
+int64_t read_scalar(spg_ctx* ctx, const int64_t* dptr);
+
+// Kernels (spgemm.cu / spgeam.cu / misc.cu)
+spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b);
+int64_t spgemm_products(spg_ctx* ctx, const spg_csr* a, const spg_csr* b);
+spg_csr* spgeam(spg_ctx* ctx, const spg_csr* a, const spg_csr* b);
+spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n);
+spg_csr* extract(spg_ctx* ctx, const spg_csr* m, int64_t r0, int64_t r1, int64_t c0, int64_t c1);
+spg_csr* copy_csr(spg_ctx* ctx, const spg_csr* m);
+void column_normalize(spg_ctx* ctx, spg_csr* m);
+spg_csr* prune(spg_ctx* ctx, const spg_csr* m, double threshold);
+void check_canonical(spg_ctx* ctx, const spg_csr* m);
+
+// Exclusive scan of n int64 counts into out[0..n] (out[n] = total). In-place allowed.
+void exclusive_scan_i64(spg_ctx* ctx, const int64_t* in, int64_t* out, int64_t n);
+
+inline int div_up(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace spgb

@@ -1,0 +1,174 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar: rowptr/colind bit-exact; values bit-exact for the local multiply (the
+kernel sums each entry in ascending k with separate mul/add, like the
+reference) and within 1e-12 relative where the summation order legitimately
+differs (trident q>=2 partial-C merge, like the reference's own trident)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2603_21444_b200 as spg
+from golden_io import csr, spgemm_cases, z
+
+pytestmark = pytest.mark.gpu
+REL_TOL = 1e-12  # north_star: fp64 values within 1e-12 relative
+
+
+def same(a, b):
+    return (int(a.nrows) == int(b.nrows) and int(a.ncols) == int(b.ncols) and np.array_equal(a.rowptr, b.rowptr)
+            and np.array_equal(np.asarray(a.colind, np.int64), np.asarray(b.colind, np.int64))
+            and np.array_equal(a.values, b.values))
+
+
+def gpu_mul(dev, a, b, check=True):
+    da, db = dev.upload(a), dev.upload(b)
+    dc = dev.spgemm(da, db)
+    if check:
+        dc.check()
+    return dc.download()
+
+
+@pytest.mark.parametrize("name", spgemm_cases())
+def test_spgemm_golden_bit_exact(dev, name):
+    c = gpu_mul(dev, csr(f"{name}_A"), csr(f"{name}_B"))
+    assert same(c, csr(f"{name}_C"))
+
+
+@pytest.mark.parametrize("n,d,seed", [(2000, 0.004, 1), (3000, 0.01, 2), (64, 0.5, 3), (1, 1.0, 1), (500, 0.2, 4)])
+def test_spgemm_random_vs_oracle(dev, n, d, seed):
+    a, b = O.port_gen_erdos_renyi(n, d, seed), O.port_gen_erdos_renyi(n, d, seed + 7)
+    assert same(gpu_mul(dev, a, b), O.port_spgemm(a, b))
+
+
+def test_config1_full_parity(dev):
+    a = spg.gen_erdos_renyi(16384, 8.0 / 16384, 1)
+    c = gpu_mul(dev, a, a)
+    ref = O.ref_spgemm_local(a, a) if O.ref_available() else O.port_spgemm(a, a)
+    assert c.nnz == 1038646
+    assert same(c, ref)
+
+
+def test_edge_cases(dev):
+    I64 = np.int64
+    # empty matrices and K = 0
+    for (m, k, n) in [(0, 0, 0), (3, 0, 4), (0, 5, 2), (4, 4, 0)]:
+        a = spg.CsrMatrix.zeros(m, k)
+        b = spg.CsrMatrix.zeros(k, n)
+        c = gpu_mul(dev, a, b)
+        assert c.nrows == m and c.ncols == n and c.nnz == 0 and len(c.rowptr) == m + 1
+    # A entries pointing at empty B rows -> zero products
+    a = spg.CsrMatrix(2, 3, np.array([0, 2, 3], I64), np.array([0, 2, 1], I64), np.array([1.0, 2.0, 3.0]))
+    b = spg.CsrMatrix(3, 2, np.array([0, 0, 1, 1], I64), np.array([1], I64), np.array([5.0]))
+    assert same(gpu_mul(dev, a, b), O.port_spgemm(a, b))
+    # ncols = 1 and explicit zero from cancellation
+    a = O.Csr(1, 2, np.array([0, 2], I64), np.array([0, 1], I64), np.array([1.0, 1.0]))
+    b = O.Csr(2, 1, np.array([0, 1, 2], I64), np.array([0, 0], I64), np.array([1.0, -1.0]))
+    c = gpu_mul(dev, a, b)
+    assert c.nnz == 1 and c.values[0] == 0.0
+    # dimension mismatch
+    with pytest.raises(spg.SpgError) as e:
+        dev.spgemm(dev.upload(spg.CsrMatrix.zeros(2, 3)), dev.upload(spg.CsrMatrix.zeros(2, 2)))
+    assert e.value.kind == "DimensionError"
+
+
+def test_heavy_and_skewed_rows(dev):
+    # a row with many entries (heavy by entries), a hub row (heavy by products),
+    # clustered columns (banded) and hub columns (many duplicates per column)
+    n = 3000
+    rng = np.random.default_rng(0)
+    rows, cols = [], []
+    rows += [0] * 2000; cols += list(rng.choice(n, 2000, replace=False))           # heavy row by entries
+    rows += list(range(1, n)); cols += list(rng.integers(0, 5, n - 1))             # hub columns 0..4
+    for i in range(1, 200):                                                        # banded block
+        for j in range(max(0, i - 20), min(n, i + 20)):
+            rows.append(i); cols.append(j)
+    vals = rng.random(len(rows)) + 0.5
+    a = O.ref_from_triplets(n, n, rows, cols, vals) if O.ref_available() else None
+    if a is None:
+        pytest.skip("needs oracle/_ref for from_triplets")
+    assert same(gpu_mul(dev, a, a), O.port_spgemm(a, a))
+    r = spg.gen_rmat(12, 16, 1, 2)
+    assert same(gpu_mul(dev, r, r), O.port_spgemm(r, r))
+
+
+def test_rectangular_and_transpose(dev):
+    a = spg.gen_erdos_renyi_rect(4096, 512, 0.01, 5)
+    at = spg.transpose(a)
+    assert same(gpu_mul(dev, a, at), O.port_spgemm(a, at))
+    assert same(gpu_mul(dev, at, a), O.port_spgemm(at, a))
+
+
+def test_products_count(dev):
+    a = spg.gen_erdos_renyi(5000, 0.002, 3)
+    assert dev.products(dev.upload(a), dev.upload(a)) == O.port_products(a, a)
+
+
+def test_spgeam_golden_and_random(dev):
+    z_ = dev.spgeam(dev.upload(csr("geam_X")), dev.upload(csr("geam_Y"))).download()
+    assert same(z_, csr("geam_Z"))
+    for n, d, s in [(1000, 0.01, 1), (100, 0.3, 2), (5, 1.0, 3), (2000, 0.05, 4)]:
+        a, b = O.port_gen_erdos_renyi(n, d, s), O.port_gen_erdos_renyi(n, d, s + 1)
+        assert same(dev.spgeam(dev.upload(a), dev.upload(b)).download(), O.port_spgeam(a, b))
+    a = O.port_gen_erdos_renyi(300, 0.1, 9)
+    neg = O.Csr(a.nrows, a.ncols, a.rowptr, a.colind, -a.values)
+    zz = dev.spgeam(dev.upload(a), dev.upload(neg)).download()
+    assert spg.pattern_equal(zz, a) and (zz.values == 0).all()
+    assert same(dev.spgeam(dev.upload(a), dev.zeros(300, 300)).download(), a)
+
+
+def test_vconcat_and_extract(dev):
+    a = spg.gen_erdos_renyi(1000, 0.01, 8)
+    da = dev.upload(a)
+    parts = [dev.extract(da, r0, r1, 0, 1000) for r0, r1 in [(0, 300), (300, 300), (300, 1000)]]
+    assert same(dev.vconcat(parts).download(), a)
+    t = dev.extract(da, 100, 700, 250, 900).download()
+    assert same(t, O.port_extract(a, np.array([100, 700, 250, 900])))
+
+
+def test_normalize_prune_bit_exact(dev):
+    m = spg.gen_erdos_renyi(3000, 0.003, 1)
+    dm = dev.upload(m)
+    dev.column_normalize(dm)
+    nm = dm.download()
+    ref = O.port_column_normalize(m)
+    assert same(nm, ref)
+    p = dev.prune(dm, 0.2).download()
+    assert same(p, O.port_prune(ref, 0.2))
+
+
+def test_determinism(dev):
+    a = spg.gen_erdos_renyi(20000, 0.0008, 11)
+    c1 = gpu_mul(dev, a, a, check=False)
+    c2 = gpu_mul(dev, a, a, check=False)
+    assert same(c1, c2)
+
+
+@pytest.mark.parametrize("P,lam", [(1, 1), (2, 2), (4, 1), (4, 4), (8, 2), (16, 4)])
+def test_trident_parity_and_ledger(P, lam):
+    a, b = csr("er300_p3_A"), csr("er300_p3_B")
+    r = spg.trident_spgemm(a, b, spg.TridentGrid.create(P, lam))
+    ref_c = csr("er300_p3_C")
+    assert spg.pattern_equal(r.c, ref_c)
+    assert spg.allclose(r.c, ref_c, REL_TOL)
+    assert np.array_equal(r.c.values, z()[f"trident_P{P}_L{lam}_Cvalues"]) or spg.allclose(
+        r.c, O.Csr(ref_c.nrows, ref_c.ncols, ref_c.rowptr, ref_c.colind, z()[f"trident_P{P}_L{lam}_Cvalues"]),
+        REL_TOL)
+    assert np.array_equal(r.ledger, z()[f"trident_P{P}_L{lam}_ledger"])
+    assert r.rounds == spg.TridentGrid.create(P, lam).q
+
+
+@pytest.mark.parametrize("P", [1, 4])
+def test_summa_parity_and_ledger(P):
+    a, b = csr("er300_p3_A"), csr("er300_p3_B")
+    r = spg.summa_spgemm(a, b, P, 2)
+    assert spg.allclose(r.c, csr("er300_p3_C"), REL_TOL)
+    assert np.array_equal(r.ledger, z()[f"summa_P{P}_ledger"])
+
+
+def test_trident_rectangular_kmer_shape():
+    a = spg.gen_erdos_renyi_rect(3000, 400, 0.01, 5)
+    at = spg.transpose(a)
+    r = spg.trident_spgemm(a, at, spg.TridentGrid.create(8, 2))
+    c = O.port_spgemm(a, at)
+    assert spg.pattern_equal(r.c, c) and spg.allclose(r.c, c, REL_TOL)

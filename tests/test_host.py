@@ -1,0 +1,116 @@
+"""CPU: host-side logic of the product (generators, tiling, ledger) against
+the reference's golden outputs and, where built, the reference itself."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2603_21444_b200 as spg
+from golden_io import csr, grids, z
+
+
+def same(a, b):
+    return (int(a.nrows) == int(b.nrows) and int(a.ncols) == int(b.ncols) and np.array_equal(a.rowptr, b.rowptr)
+            and np.array_equal(a.colind, b.colind) and np.array_equal(a.values, b.values))
+
+
+def test_generator_bit_exact_vs_golden():
+    for s in (1, 2, 3):
+        assert same(spg.gen_erdos_renyi(40, 0.15, s), csr(f"er40_s{s}_A"))
+    assert same(spg.gen_erdos_renyi(3, 0.7, 11), csr("identity3_B"))
+    assert same(spg.gen_erdos_renyi(20, 1.0, 4), csr("dense20_A"))
+    assert same(spg.gen_erdos_renyi(300, 0.03, 3), csr("er300_p3_A"))
+
+
+@pytest.mark.parametrize("n,d,seed", [(16384, 8.0 / 16384, 1), (5000, 0.001, 9), (100, 0.5, 3), (0, 0.1, 1), (7, 1.0, 2)])
+def test_generator_bit_exact_vs_port(n, d, seed):
+    assert same(spg.gen_erdos_renyi(n, d, seed), O.port_gen_erdos_renyi(n, d, seed))
+
+
+def test_generator_errors():
+    for bad in [(10, 0.0, 1), (10, 1.5, 1), (-1, 0.5, 1)]:
+        with pytest.raises(spg.SpgError):
+            spg.gen_erdos_renyi(*bad)
+
+
+def test_rect_generator_matches_port_and_transpose():
+    a = spg.gen_erdos_renyi_rect(1000, 300, 0.01, 5)
+    assert same(a, O.port_gen_erdos_renyi_rect(1000, 300, 0.01, 5))
+    t = spg.transpose(a)
+    assert t.is_canonical() and t.nrows == 300 and t.ncols == 1000
+    d = np.zeros((1000, 300))
+    for i in range(1000):
+        d[i, a.colind[a.rowptr[i]:a.rowptr[i + 1]]] = a.values[a.rowptr[i]:a.rowptr[i + 1]]
+    dt = np.zeros((300, 1000))
+    for i in range(300):
+        dt[i, t.colind[t.rowptr[i]:t.rowptr[i + 1]]] = t.values[t.rowptr[i]:t.rowptr[i + 1]]
+    assert np.array_equal(d.T, dt)
+
+
+def test_rmat_deterministic_and_canonical():
+    a = spg.gen_rmat(10, 8, 1, 2)
+    b = spg.gen_rmat(10, 8, 1, 2)
+    assert same(a, b)
+    a.check_canonical()
+    assert a.nrows == 1024 and 0 < a.nnz <= 8 * 1024
+    assert not same(a, spg.gen_rmat(10, 8, 3, 2))
+
+
+@pytest.mark.parametrize("P,lam", grids())
+def test_partition_matches_reference(P, lam):
+    a = csr("er300_p3_A")
+    tiles, tm = spg.partition(a, "trident", P, lam)
+    assert np.array_equal(tm.tiles, z()[f"part_P{P}_L{lam}_rects"])
+    assert [t.nnz for t in tiles] == z()[f"part_P{P}_L{lam}_nnz"].tolist()
+    assert same(spg.reassemble(tiles, tm), a)
+
+
+def test_tile_map_spec_pins():
+    tm = spg.make_tile_map(8, 8, "trident", 16, 4)
+    assert tm.row_bounds.tolist() == list(range(9)) and tm.col_bounds.tolist() == [0, 4, 8]
+    assert spg.block_bounds(10, 3).tolist() == [0, 4, 7, 10]
+    tm = spg.make_tile_map(2, 5, "trident", 16, 4)  # zero-row slices
+    assert (tm.tiles[:, 1] - tm.tiles[:, 0]).min() == 0
+    with pytest.raises(spg.SpgError):
+        spg.make_tile_map(4, 4, "grid2d", 8, 1)
+
+
+def test_reassemble_rejects_bad_tiles():
+    a = csr("er300_p3_A")
+    tiles, tm = spg.partition(a, "trident", 4, 1)
+    with pytest.raises(spg.SpgError) as e:
+        spg.reassemble(tiles[:3], tm)
+    assert e.value.kind == "IncompleteTileSet"
+
+
+@pytest.mark.parametrize("P,lam", grids())
+def test_trident_ledger_matches_reference(P, lam):
+    a, b = csr("er300_p3_A"), csr("er300_p3_B")
+    g = spg.TridentGrid.create(P, lam)
+    ta, _ = spg.partition(a, "trident", P, lam)
+    tb, _ = spg.partition(b, "trident", P, lam)
+    L = spg.trident_ledger(g, [(t.nrows, t.nnz) for t in ta], [(t.nrows, t.nnz) for t in tb])
+    assert np.array_equal(L, z()[f"trident_P{P}_L{lam}_ledger"])
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_prop1_exactness_uniform_stride():
+    # uniform stride at P=16, lambda=4: GI recv per rank = 2(q-1)nnz/P
+    n, k = 256, 16
+    rows = np.repeat(np.arange(n), k)
+    cols = ((np.arange(n)[:, None] + np.arange(k)[None, :] * (n // k)) % n).ravel()
+    vals = 1.0 + ((rows + cols) % 7) * 0.125
+    a = O.ref_from_triplets(n, n, rows, cols, vals)
+    g = spg.TridentGrid.create(16, 4)
+    ta, _ = spg.partition(a, "trident", 16, 4)
+    L = spg.trident_ledger(g, [(t.nrows, t.nnz) for t in ta], [(t.nrows, t.nnz) for t in ta])
+    ref = O.ref_run_algo("trident", a, a, 16, 4, want_c=False)["ledger"]
+    assert np.array_equal(L, ref)
+    assert (L[:, 1, 1, 1] == 512).all() and (L[:, 1, 0, 1] == 1536).all()
+
+
+def test_csr_canonical_checker():
+    m = spg.CsrMatrix(2, 2, np.array([0, 2, 2]), np.array([0, 0]), np.ones(2))
+    assert not m.is_canonical()
+    m = spg.CsrMatrix(2, 2, np.array([0, 1, 1]), np.array([5]), np.ones(1))
+    assert not m.is_canonical()
+    assert spg.gen_erdos_renyi(50, 0.2, 1).is_canonical()
