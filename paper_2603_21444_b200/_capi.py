@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libspgb200.so")
+LIB_PATH = os.environ.get("SPG_LIB_PATH") or os.path.join(_HERE, "lib", "libspgb200.so")
 CXX_LIB_PATH = os.path.join(_HERE, "lib", "libspgsim_b200.so")
 
 # Every symbol declared in include/spg/capi.h (checked by tests/test_capi_symbols.py).

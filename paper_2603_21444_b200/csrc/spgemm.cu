@@ -32,82 +32,382 @@
 namespace spgb {
 namespace {
 
-constexpr int NT = 256;              // threads per tile CTA
-constexpr int TILE_H = 1024;         // product half-capacity (tile ≤ 2*TILE_H)
-constexpr int TILE_P = 2 * TILE_H;   // product capacity
-constexpr int TILE_RH = 128;         // rows per tile ≤ TILE_RH
-constexpr int TILE_EH = 256;         // A entries per tile ≤ 2*TILE_EH
-constexpr int TILE_E = 2 * TILE_EH;
-constexpr int BUCKET_LOAD = 2;       // target products per bucket
-constexpr int NB_MAX = TILE_P / BUCKET_LOAD + TILE_RH;
+// ----------------------------------------------------------- row classes
+// WARP rows: ≤ 32 A entries and ≤ WARP_P products — one warp per row, the
+// products live in registers, one bucket-sorted copy in the warp's smem slice.
+// CTA rows: ≤ CTA_E entries and ≤ CTA_P products — one CTA per row in smem.
+// HEAVY rows: the rest — one CTA per row with the arrays in global memory.
+#ifndef SPG_WARP_MINB
+#define SPG_WARP_MINB 3
+#endif
+constexpr int WARP_NJ = 16;                // products per lane
+constexpr int WARP_P = 32 * WARP_NJ;       // 512
+constexpr int NT = 256;                    // threads per CTA
+constexpr int CTA_P = 4096;
+constexpr int CTA_E = 1024;
+constexpr int BUCKET_LOAD = 2;             // target products per bucket
+constexpr int CTA_NB = CTA_P / BUCKET_LOAD + 1;
 
-struct TileSmem {
-    int32_t col[TILE_P];
-    double val[TILE_P];
-    uint16_t bkt[TILE_P];
-    uint16_t perm[TILE_P];
-    int64_t e_bst[TILE_E];
-    double e_av[TILE_E];
-    int32_t e_pre[TILE_E + 1];
-    uint8_t e_row[TILE_E];
-    int32_t r_pbase[TILE_RH + 1];
-    int32_t r_bbase[TILE_RH + 1];
-    int32_t r_minc[TILE_RH];
-    int32_t r_maxc[TILE_RH];
-    float r_scale[TILE_RH];
-    int32_t b_off[NB_MAX + 1];
-    int32_t b_cnt[NB_MAX + 1];
-    int32_t ws[NT / 32 + 1];
-};
+enum RowClass : int8_t { RC_EMPTY = 0, RC_WARP = 1, RC_CTA = 2, RC_HEAVY = 3 };
 
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 
 // ------------------------------------------------------------ row products
+// products(i) = Σ_{k∈A_i} nnz(B_k); rows outside the warp class are appended
+// to the CTA / heavy lists.
 __global__ void k_row_products(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
-                               const int64_t* __restrict__ brp, int64_t m, int64_t* __restrict__ prod) {
+                               const int64_t* __restrict__ brp, int64_t m, int64_t* __restrict__ prod,
+                               int32_t* __restrict__ cta_list, int32_t* __restrict__ heavy_list,
+                               int32_t* __restrict__ counts) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
         int64_t p = 0;
-        const int64_t e1 = arp[i + 1];
-        for (int64_t e = arp[i]; e < e1; ++e) {
+        const int64_t e0 = arp[i], e1 = arp[i + 1];
+        for (int64_t e = e0; e < e1; ++e) {
             const int32_t k = __ldg(acol + e);
             p += __ldg(brp + k + 1) - __ldg(brp + k);
         }
         prod[i] = p;
+        const int64_t ne = e1 - e0;
+        if (p == 0 || (ne <= 32 && p <= WARP_P)) continue;
+        if (ne <= CTA_E && p <= CTA_P) cta_list[atomicAdd(counts + 0, 1)] = static_cast<int32_t>(i);
+        else heavy_list[atomicAdd(counts + 1, 1)] = static_cast<int32_t>(i);
     }
 }
 
-__device__ __forceinline__ bool row_is_heavy(int64_t prod, int64_t nent) {
-    return prod > TILE_H || nent > TILE_EH;
+// Monotone map column -> [0, nb): high bits of the column scaled by nb.
+__device__ __forceinline__ int bucket_of(uint32_t col, int cshift, int nb) {
+    return static_cast<int>(__umulhi(col << cshift, static_cast<uint32_t>(nb)));
 }
 
-__device__ __forceinline__ int64_t tile_key(int64_t i, const int64_t* pex, const int64_t* arp) {
-    return pex[i] / TILE_H + i / TILE_RH + arp[i] / TILE_EH;
+// Warp-cooperative A-row setup. The row's entries whose B row is nonempty are
+// compacted onto lanes 0..mn-1 (ascending k); lane t holds base_t = (B row
+// start) - (product prefix), so product x of entry t sits at B position base_t + x.
+struct RowEntries {
+    int64_t base;
+    double av;
+    int pre;  // exclusive product prefix; INT_MAX on lanes >= mn
+    int p;    // products of the row
+};
+
+template <bool VALS>
+__device__ __forceinline__ RowEntries load_row(const int32_t* __restrict__ acol, const double* __restrict__ aval,
+                                               const int64_t* __restrict__ brp, int64_t e0, int m, int lane) {
+    int len = 0;
+    int64_t bs = 0;
+    double av = 0.0;
+    if (lane < m) {
+        const int32_t k = __ldg(acol + e0 + lane);
+        if (VALS) av = __ldg(aval + e0 + lane);
+        bs = __ldg(brp + k);
+        len = static_cast<int>(__ldg(brp + k + 1) - bs);
+    }
+    const unsigned nz = __ballot_sync(0xffffffffu, len > 0);
+    const int mn = __popc(nz);
+    const int src = static_cast<int>(__fns(nz, 0, lane + 1)) & 31;
+    int lc = __shfl_sync(0xffffffffu, len, src);
+    const int64_t bc = __shfl_sync(0xffffffffu, bs, src);
+    RowEntries r;
+    r.av = VALS ? __shfl_sync(0xffffffffu, av, src) : 0.0;
+    if (lane >= mn) lc = 0;
+    int inc = lc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    r.p = __shfl_sync(0xffffffffu, inc, 31);
+    const int pre = inc - lc;
+    r.base = bc - pre;
+    r.pre = lane < mn ? pre : INT_MAX;
+    return r;
 }
 
-// flags[i] = 1 when row i starts a tile; heavy rows appended to heavy_list.
-__global__ void k_tile_flags(const int64_t* __restrict__ pex, const int64_t* __restrict__ arp, int64_t m,
-                             int32_t* __restrict__ flags, int32_t* __restrict__ heavy_list,
-                             int32_t* __restrict__ heavy_count) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
-        flags[i] = (i == 0 || tile_key(i, pex, arp) != tile_key(i - 1, pex, arp)) ? 1 : 0;
-        if (row_is_heavy(pex[i + 1] - pex[i], arp[i + 1] - arp[i])) {
-            const int slot = atomicAdd(heavy_count, 1);
-            heavy_list[slot] = static_cast<int32_t>(i);
+// Entry of product x = 32*j + lane: t0 = entry covering 32*j (ballot), plus the
+// entries that start inside the chunk before x (one OR-reduction of start bits).
+__device__ __forceinline__ int chunk_entry(int pre, int j, int lane) {
+    const int c0 = 32 * j;
+    const int t0 = __popc(__ballot_sync(0xffffffffu, pre <= c0)) - 1;
+    const int rel = pre - c0;
+    const unsigned sm = __reduce_or_sync(0xffffffffu, (rel > 0 && rel < 32) ? (1u << rel) : 0u);
+    return t0 + __popc(sm & ((2u << lane) - 1u));
+}
+
+// Per-warp smem slice of the numeric kernel: products in bucket order plus
+// 16-bit bucket counters / offsets packed two per word (2p buckets, p ≤ 512).
+constexpr int WARP_NB = 2 * WARP_P;
+struct WarpSlice {
+    int32_t col[WARP_P];
+    double val[WARP_P];
+    uint16_t x[WARP_P];
+    uint32_t offw[WARP_NB / 2 + 1];
+};
+
+__device__ __forceinline__ int off16(const uint32_t* offw, int b) {
+    return static_cast<int>((offw[b >> 1] >> ((b & 1) << 4)) & 0xffffu);
+}
+
+// --------------------------------------------------------- warp symbolic
+// Distinct columns per row via an open-addressing set in the warp's smem.
+constexpr int SYM_T = 2 * WARP_P;
+template <int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_warp_symbolic(const int64_t* __restrict__ arp,
+                                                            const int32_t* __restrict__ acol,
+                                                            const int64_t* __restrict__ brp,
+                                                            const int32_t* __restrict__ bcol, int64_t m,
+                                                            int64_t* __restrict__ row_nnz) {
+    __shared__ int32_t table[WPB][SYM_T];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int32_t* tab = table[w];
+    const int64_t gw = blockIdx.x * int64_t(WPB) + w, nw = int64_t(gridDim.x) * WPB;
+    for (int64_t i = gw; i < m; i += nw) {
+        const int64_t e0 = arp[i];
+        const int ne = static_cast<int>(arp[i + 1] - e0);
+        if (ne == 0 || ne > 32) continue;
+        const RowEntries re = load_row<false>(acol, nullptr, brp, e0, ne, lane);
+        const int p = re.p;
+        if (p == 0 || p > WARP_P) continue;
+        int lg = 6;
+        while ((1 << lg) < 2 * p) ++lg;
+        const int T = 1 << lg;
+        for (int q = lane; q < T; q += 32) tab[q] = -1;
+        __syncwarp();
+        int32_t cols[WARP_NJ];
+#pragma unroll
+        for (int j = 0; j < WARP_NJ; ++j) {
+            cols[j] = -1;
+            if (j * 32 < p) {
+                const int t = chunk_entry(re.pre, j, lane);
+                const int64_t base = __shfl_sync(0xffffffffu, re.base, t);
+                const int x = 32 * j + lane;
+                if (x < p) cols[j] = __ldg(bcol + base + x);
+            }
         }
+        int fresh = 0;
+#pragma unroll
+        for (int j = 0; j < WARP_NJ; ++j) {
+            if (cols[j] < 0) continue;
+            uint32_t h = (static_cast<uint32_t>(cols[j]) * 0x9E3779B1u) >> (32 - lg);
+            while (true) {
+                const int32_t old = atomicCAS(&tab[h], -1, cols[j]);
+                if (old == -1) { ++fresh; break; }
+                if (old == cols[j]) break;
+                h = (h + 1) & (T - 1);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) fresh += __shfl_xor_sync(0xffffffffu, fresh, o);
+        if (lane == 0) row_nnz[i] = fresh;
+        __syncwarp();
     }
 }
 
-__global__ void k_tile_scatter(const int32_t* __restrict__ flags, const int64_t* __restrict__ pos, int64_t m,
-                               int32_t* __restrict__ tile_start) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
-        if (flags[i]) tile_start[pos[i]] = static_cast<int32_t>(i);
-        if (i == m - 1) tile_start[pos[m]] = static_cast<int32_t>(m);
+// ---------------------------------------------------------- warp numeric
+// Products are gathered into registers (x = 32j + lane, ascending k within the
+// row), counted into ~p/2 column buckets, and scattered once into the warp's
+// smem slice in bucket order. Each lane then sorts its buckets (≈2 entries) in
+// place by (col, x): the slice holds the row sorted by column and is copied to
+// C with coalesced stores. Rows with duplicate columns combine each run of
+// equal columns in x order (= ascending k, separate mul and add), so values are
+// bit-identical to the reference.
+template <int WPB>
+__global__ void __launch_bounds__(WPB * 32, SPG_WARP_MINB) k_warp_numeric(const int64_t* __restrict__ arp,
+                                                           const int32_t* __restrict__ acol,
+                                                           const double* __restrict__ aval,
+                                                           const int64_t* __restrict__ brp,
+                                                           const int32_t* __restrict__ bcol,
+                                                           const double* __restrict__ bval, int64_t m, int cshift,
+                                                           const int64_t* __restrict__ crp, int32_t* __restrict__ ccol,
+                                                           double* __restrict__ cval) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    WarpSlice& S = reinterpret_cast<WarpSlice*>(smem_raw)[w];
+    const int64_t gw = blockIdx.x * int64_t(WPB) + w, nw = int64_t(gridDim.x) * WPB;
+    for (int64_t i = gw; i < m; i += nw) {
+        const int64_t e0 = arp[i];
+        const int ne = static_cast<int>(arp[i + 1] - e0);
+        if (ne == 0 || ne > 32) continue;
+        const RowEntries re = load_row<true>(acol, aval, brp, e0, ne, lane);
+        const int p = re.p;
+        if (p == 0 || p > WARP_P) continue;
+        const int nb = 2 * p;          // ~0.5 products per bucket
+        const int nw = (nb + 2) >> 1;  // packed words incl. the off[nb] slot
+        for (int q = lane; q < nw; q += 32) S.offw[q] = 0u;
+
+        // expand: every gather issued before any is consumed
+        int32_t col[WARP_NJ];
+        double val[WARP_NJ];
+        int ent[WARP_NJ];
+#pragma unroll
+        for (int j = 0; j < WARP_NJ; ++j) {
+            col[j] = 0;
+            val[j] = 0.0;
+            ent[j] = 0;
+            if (j * 32 < p) {
+                const int t = chunk_entry(re.pre, j, lane);
+                const int64_t base = __shfl_sync(0xffffffffu, re.base, t);
+                ent[j] = t;
+                const int x = 32 * j + lane;
+                if (x < p) {
+                    col[j] = __ldg(bcol + base + x);
+                    val[j] = __ldg(bval + base + x);
+                }
+            }
+        }
+        __syncwarp();
+        int slot[WARP_NJ];
+#pragma unroll
+        for (int j = 0; j < WARP_NJ; ++j) {
+            slot[j] = -1;
+            if (j * 32 < p) {
+                const double a = __shfl_sync(0xffffffffu, re.av, ent[j]);
+                if (32 * j + lane < p) {
+                    val[j] = dmul(a, val[j]);
+                    const int b = bucket_of(col[j], cshift, nb);
+                const int sh = (b & 1) << 4;
+                    slot[j] = static_cast<int>((atomicAdd(&S.offw[b >> 1], 1u << sh) >> sh) & 0xffffu);
+                }
+            }
+        }
+        __syncwarp();
+        // exclusive scan of the 16-bit counts (contiguous words per lane)
+        {
+            constexpr int PERW = (WARP_NB / 2 + 1 + 31) / 32;
+            uint32_t wv[PERW];
+            int s = 0;
+#pragma unroll
+            for (int q = 0; q < PERW; ++q) {
+                const int wi = lane * PERW + q;
+                wv[q] = wi < nw ? S.offw[wi] : 0u;
+                s += static_cast<int>((wv[q] & 0xffffu) + (wv[q] >> 16));
+            }
+            int inc = s;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            uint32_t pre = static_cast<uint32_t>(inc - s);
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < PERW; ++q) {
+                const int wi = lane * PERW + q;
+                const uint32_t lo = pre, hi = pre + (wv[q] & 0xffffu);
+                if (wi < nw) S.offw[wi] = lo | (hi << 16);
+                pre = hi + (wv[q] >> 16);
+            }
+        }
+        __syncwarp();
+        // scatter into bucket order
+#pragma unroll
+        for (int j = 0; j < WARP_NJ; ++j) {
+            if (slot[j] >= 0) {
+                const int pos = off16(S.offw, bucket_of(col[j], cshift, nb)) + slot[j];
+                S.col[pos] = col[j];
+                S.val[pos] = val[j];
+                S.x[pos] = static_cast<uint16_t>(32 * j + lane);
+            }
+        }
+        __syncwarp();
+        // order each bucket by (col, x): pairs in one uniform pass, larger
+        // buckets (rare at 0.5 products/bucket) by their first lane
+        bool dup = false;
+        unsigned big = 0;  // bit i: position lane+32i starts a bucket of >= 3
+        for (int q0 = 0; q0 < p; q0 += 32) {
+            const int q = q0 + lane;
+            if (q < p) {
+                const int32_t c = S.col[q];
+                const int bb = bucket_of(c, cshift, nb);
+                const int lo = off16(S.offw, bb), hi = off16(S.offw, bb + 1);
+                if (q == lo && hi - lo == 2) {
+                    const int32_t c2 = S.col[q + 1];
+                    const uint16_t x1 = S.x[q], x2 = S.x[q + 1];
+                    dup |= c2 == c;
+                    if (c2 < c || (c2 == c && x2 < x1)) {
+                        const double v1 = S.val[q];
+                        S.col[q] = c2;
+                        S.col[q + 1] = c;
+                        S.val[q] = S.val[q + 1];
+                        S.val[q + 1] = v1;
+                        S.x[q] = x2;
+                        S.x[q + 1] = x1;
+                    }
+                } else if (q == lo && hi - lo > 2) {
+                    big |= 1u << (q0 >> 5);
+                }
+            }
+        }
+        while (big) {
+            const int q = lane + 32 * (__ffs(big) - 1);
+            big &= big - 1;
+            const int bb = bucket_of(S.col[q], cshift, nb);
+            const int lo = q, hi = off16(S.offw, bb + 1);
+            for (int a = lo + 1; a < hi; ++a) {
+                const int32_t ca = S.col[a];
+                const double va = S.val[a];
+                const uint16_t xa = S.x[a];
+                int r = a - 1;
+                while (r >= lo && (S.col[r] > ca || (S.col[r] == ca && S.x[r] > xa))) {
+                    S.col[r + 1] = S.col[r];
+                    S.val[r + 1] = S.val[r];
+                    S.x[r + 1] = S.x[r];
+                    --r;
+                }
+                S.col[r + 1] = ca;
+                S.val[r + 1] = va;
+                S.x[r + 1] = xa;
+            }
+            for (int a = lo + 1; a < hi; ++a) dup |= S.col[a] == S.col[a - 1];
+        }
+        __syncwarp();
+        const int64_t obase = crp[i];
+        if (!__any_sync(0xffffffffu, dup)) {
+            for (int q = lane; q < p; q += 32) {
+                ccol[obase + q] = S.col[q];
+                cval[obase + q] = dadd(0.0, S.val[q]);
+            }
+        } else {
+            // runs of equal columns, already in ascending x (= ascending k)
+            int out = 0;
+            for (int base = 0; base < p; base += 32) {
+                const int q = base + lane;
+                const bool head = q < p && (q == 0 || S.col[q] != S.col[q - 1]);
+                const unsigned hm = __ballot_sync(0xffffffffu, head);
+                if (head) {
+                    const int32_t c = S.col[q];
+                    double sum = dadd(0.0, S.val[q]);
+                    for (int u = q + 1; u < p && S.col[u] == c; ++u) sum = dadd(sum, S.val[u]);
+                    const int o = out + __popc(hm & ((1u << lane) - 1));
+                    ccol[obase + o] = c;
+                    cval[obase + o] = sum;
+                }
+                out += __popc(hm);
+            }
+        }
+        __syncwarp();
     }
 }
 
-// Monotone map of a column into the row's bucket range.
-__device__ __forceinline__ int bucket_of(int32_t col, int32_t minc, float scale, int nb) {
+// ---------------------------------------------------------------- CTA rows
+// One CTA per row (≤ CTA_P products, ≤ CTA_E entries): the same bucketed ESC
+// with the product arrays in shared memory and block-wide phases.
+struct CtaSmem {
+    int32_t col[CTA_P];
+    double val[CTA_P];
+    uint16_t bkt[CTA_P];
+    uint16_t perm[CTA_P];
+    int64_t e_bst[CTA_E];
+    double e_av[CTA_E];
+    int32_t e_pre[CTA_E + 1];
+    int32_t b_off[CTA_NB + 1];
+    int32_t b_cnt[CTA_NB + 1];
+    int32_t ws[NT / 32 + 1];
+    int32_t minc, maxc;
+    float scale;
+};
+
+// Monotone map of a column into [0, nb) over the row's [minc, maxc] range.
+__device__ __forceinline__ int bucket_range(int32_t col, int32_t minc, float scale, int nb) {
     int b = static_cast<int>(static_cast<float>(col - minc) * scale);
     return b < nb - 1 ? b : nb - 1;
 }
@@ -139,45 +439,31 @@ __device__ __forceinline__ int sort_bucket(PermT* perm, int64_t lo, int64_t hi, 
     return u;
 }
 
-// --------------------------------------------------------------- tile kernel
 template <bool NUMERIC>
-__global__ void __launch_bounds__(NT) k_tile(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
-                                             const double* __restrict__ aval, const int64_t* __restrict__ brp,
-                                             const int32_t* __restrict__ bcol, const double* __restrict__ bval,
-                                             const int64_t* __restrict__ pex, const int32_t* __restrict__ tile_start,
-                                             int ntiles, int64_t* __restrict__ row_nnz,
-                                             const int64_t* __restrict__ crp, int32_t* __restrict__ ccol,
-                                             double* __restrict__ cval) {
+__global__ void __launch_bounds__(NT) k_cta_rows(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
+                                                 const double* __restrict__ aval, const int64_t* __restrict__ brp,
+                                                 const int32_t* __restrict__ bcol, const double* __restrict__ bval,
+                                                 const int64_t* __restrict__ prod, const int32_t* __restrict__ rows,
+                                                 const int32_t* __restrict__ nrows_dev, int64_t* __restrict__ row_nnz,
+                                                 const int64_t* __restrict__ crp, int32_t* __restrict__ ccol,
+                                                 double* __restrict__ cval) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    TileSmem& s = *reinterpret_cast<TileSmem*>(smem_raw);
+    CtaSmem& s = *reinterpret_cast<CtaSmem*>(smem_raw);
     const int tid = threadIdx.x;
-
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int64_t r0 = tile_start[t];
-        const int64_t r1 = tile_start[t + 1];
-        int64_t rl1 = r1;  // end of light rows; a heavy row can only be last
-        if (row_is_heavy(pex[r1] - pex[r1 - 1], arp[r1] - arp[r1 - 1])) rl1 = r1 - 1;
-        const int nr = static_cast<int>(rl1 - r0);
-        if (nr <= 0) continue;
-        const int64_t e0 = arp[r0];
-        const int ne = static_cast<int>(arp[rl1] - e0);
-        const int64_t pbase0 = pex[r0];
-        const int ptile = static_cast<int>(pex[rl1] - pbase0);
-
-        // P0: row metadata, entry -> row map
-        for (int r = tid; r < nr; r += NT) {
-            s.r_pbase[r] = static_cast<int32_t>(pex[r0 + r] - pbase0);
-            s.r_minc[r] = INT_MAX;
-            s.r_maxc[r] = -1;
-            const int ea = static_cast<int>(arp[r0 + r] - e0), eb = static_cast<int>(arp[r0 + r + 1] - e0);
-            for (int e = ea; e < eb; ++e) s.e_row[e] = static_cast<uint8_t>(r);
+    const int nrows = *nrows_dev;
+    for (int t = blockIdx.x; t < nrows; t += gridDim.x) {
+        const int64_t i = rows[t];
+        const int64_t e0 = arp[i];
+        const int ne = static_cast<int>(arp[i + 1] - e0);
+        const int ptile = static_cast<int>(prod[i]);
+        if (tid == 0) {
+            s.minc = INT_MAX;
+            s.maxc = -1;
         }
-        if (tid == 0) s.r_pbase[nr] = ptile;
         __syncthreads();
-
-        // P1: A entries -> B row spans, column range per row, product prefix
+        // A entries -> B row spans, column range, product prefix
         {
-            constexpr int EI = TILE_E / NT;
+            constexpr int EI = CTA_E / NT;
             int lens[EI];
             int sum = 0;
 #pragma unroll
@@ -191,9 +477,8 @@ __global__ void __launch_bounds__(NT) k_tile(const int64_t* __restrict__ arp, co
                     s.e_av[e] = aval[e0 + e];
                     lens[q] = static_cast<int>(be - bs);
                     if (be > bs) {
-                        const int r = s.e_row[e];
-                        atomicMin(&s.r_minc[r], bcol[bs]);
-                        atomicMax(&s.r_maxc[r], bcol[be - 1]);
+                        atomicMin(&s.minc, bcol[bs]);
+                        atomicMax(&s.maxc, bcol[be - 1]);
                     }
                 }
                 sum += lens[q];
@@ -208,75 +493,48 @@ __global__ void __launch_bounds__(NT) k_tile(const int64_t* __restrict__ arp, co
             }
             if (tid == 0) s.e_pre[ne] = total;
         }
+        const int nb = (ptile + BUCKET_LOAD - 1) / BUCKET_LOAD;
+        for (int b = tid; b <= nb; b += NT) s.b_cnt[b] = 0;
         __syncthreads();
-
-        // P2: bucket ranges per row
-        {
-            int nb = 0;
-            if (tid < nr) {
-                const int pr = s.r_pbase[tid + 1] - s.r_pbase[tid];
-                nb = (pr + BUCKET_LOAD - 1) / BUCKET_LOAD;
-                if (pr > 0) {
-                    const int64_t range = int64_t(s.r_maxc[tid]) - s.r_minc[tid] + 1;
-                    s.r_scale[tid] = static_cast<float>(nb) / static_cast<float>(range);
-                }
-            }
-            static_assert(TILE_RH <= NT, "one thread per row");
-            int total;
-            const int pre = block_exclusive_scan<NT>(nb, &total, s.ws);
-            if (tid < nr) s.r_bbase[tid] = pre;
-            if (tid == 0) s.r_bbase[nr] = total;
-            for (int b = tid; b <= total; b += NT) s.b_cnt[b] = 0;
-        }
+        if (tid == 0) s.scale = static_cast<float>(nb) / static_cast<float>(int64_t(s.maxc) - s.minc + 1);
         __syncthreads();
-        const int nbt = s.r_bbase[nr];
+        const int32_t minc = s.minc;
+        const float scale = s.scale;
 
-        // P3: expand products into smem and count buckets
         for (int x = tid; x < ptile; x += NT) {
             int lo = 0, hi = ne;  // largest e with e_pre[e] <= x
             while (hi - lo > 1) {
                 const int mid = (lo + hi) >> 1;
                 if (s.e_pre[mid] <= x) lo = mid; else hi = mid;
             }
-            const int e = lo;
-            const int64_t u = s.e_bst[e] + (x - s.e_pre[e]);
+            const int64_t u = s.e_bst[lo] + (x - s.e_pre[lo]);
             const int32_t c = bcol[u];
-            const int r = s.e_row[e];
-            const int nb = s.r_bbase[r + 1] - s.r_bbase[r];
-            const int b = s.r_bbase[r] + bucket_of(c, s.r_minc[r], s.r_scale[r], nb);
+            const int b = bucket_range(c, minc, scale, nb);
             s.col[x] = c;
             s.bkt[x] = static_cast<uint16_t>(b);
-            if (NUMERIC) s.val[x] = dmul(s.e_av[e], bval[u]);
+            if (NUMERIC) s.val[x] = dmul(s.e_av[lo], bval[u]);
             atomicAdd(&s.b_cnt[b], 1);
         }
         __syncthreads();
-
-        // P4: bucket offsets
-        block_scan_array<NT, (NB_MAX + NT) / NT, int32_t>(s.b_cnt, nbt, s.ws);
-        for (int b = tid; b <= nbt; b += NT) {
+        block_scan_array<NT, (CTA_NB + NT) / NT, int32_t>(s.b_cnt, nb, s.ws);
+        for (int b = tid; b <= nb; b += NT) {
             s.b_off[b] = s.b_cnt[b];
             s.b_cnt[b] = 0;
         }
         __syncthreads();
-
-        // P5: scatter product ids into buckets
         for (int x = tid; x < ptile; x += NT) {
             const int b = s.bkt[x];
-            const int pos = s.b_off[b] + atomicAdd(&s.b_cnt[b], 1);
-            s.perm[pos] = static_cast<uint16_t>(x);
+            s.perm[s.b_off[b] + atomicAdd(&s.b_cnt[b], 1)] = static_cast<uint16_t>(x);
         }
         __syncthreads();
-
-        // P6: sort each bucket by (col, x); count distinct columns
-        for (int b = tid; b < nbt; b += NT) s.b_cnt[b] = sort_bucket(s.perm, s.b_off[b], s.b_off[b + 1], s.col);
+        for (int b = tid; b < nb; b += NT) s.b_cnt[b] = sort_bucket(s.perm, s.b_off[b], s.b_off[b + 1], s.col);
         __syncthreads();
-        block_scan_array<NT, (NB_MAX + NT) / NT, int32_t>(s.b_cnt, nbt, s.ws);  // -> unique offsets
-
+        block_scan_array<NT, (CTA_NB + NT) / NT, int32_t>(s.b_cnt, nb, s.ws);
         if (!NUMERIC) {
-            for (int r = tid; r < nr; r += NT) row_nnz[r0 + r] = s.b_cnt[s.r_bbase[r + 1]] - s.b_cnt[s.r_bbase[r]];
+            if (tid == 0) row_nnz[i] = s.b_cnt[nb];
         } else {
-            const int64_t obase = crp[r0];
-            for (int b = tid; b < nbt; b += NT) {
+            const int64_t obase = crp[i];
+            for (int b = tid; b < nb; b += NT) {
                 int64_t o = obase + s.b_cnt[b];
                 const int lo = s.b_off[b], hi = s.b_off[b + 1];
                 int a = lo;
@@ -450,11 +708,24 @@ int64_t spgemm_products(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     const int64_t m = a->nrows;
     if (m == 0 || a->nnz == 0) return 0;
     DBuf<int64_t> prod(ctx, m), pex(ctx, m + 1);
-    k_row_products<<<grid_for(ctx, m), 256, 0, ctx->stream>>>(a->rowptr, a->colind, b->rowptr, m, prod);
+    DBuf<int32_t> lists(ctx, 2 * m), counts(ctx, 2);
+    SPG_CUDA(cudaMemsetAsync(counts.get(), 0, 2 * sizeof(int32_t), ctx->stream));
+    k_row_products<<<grid_for(ctx, m), 256, 0, ctx->stream>>>(a->rowptr, a->colind, b->rowptr, m, prod, lists,
+                                                              lists.get() + m, counts);
     SPG_LAUNCH_CHECK();
     exclusive_scan_i64(ctx, prod, pex, m);
     return read_scalar(ctx, pex.get() + m);
 }
+
+namespace {
+constexpr int WPB = 8;  // warps per block of the warp kernels
+
+int cshift_for(int64_t ncols) {
+    int bits = 1;
+    while ((int64_t(1) << bits) < ncols) ++bits;
+    return 32 - bits;  // col << cshift puts the top column bit at bit 31
+}
+}  // namespace
 
 spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     if (a->ncols != b->nrows)
@@ -462,74 +733,42 @@ spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
              "spgemm: a.ncols=" + std::to_string(a->ncols) + " != b.nrows=" + std::to_string(b->nrows));
     const int64_t m = a->nrows, n = b->ncols;
     if (m == 0 || a->nnz == 0 || b->nnz == 0) return new_csr(ctx, m, n, 0);
+    const int cshift = cshift_for(n);
 
-    // 1-2: products per row and their prefix
-    DBuf<int64_t> prod(ctx, m), pex(ctx, m + 1);
+    // 1: products per row + CTA/heavy row lists
+    DBuf<int64_t> prod(ctx, m);
+    DBuf<int32_t> lists(ctx, 2 * m), counts(ctx, 2);
+    int32_t* cta_list = lists.get();
+    int32_t* heavy_list = lists.get() + m;
+    SPG_CUDA(cudaMemsetAsync(counts.get(), 0, 2 * sizeof(int32_t), ctx->stream));
     {
         KTime kt(ctx, "row_products");
-        k_row_products<<<grid_for(ctx, m), 256, 0, ctx->stream>>>(a->rowptr, a->colind, b->rowptr, m, prod);
+        k_row_products<<<grid_for(ctx, m), 256, 0, ctx->stream>>>(a->rowptr, a->colind, b->rowptr, m, prod, cta_list,
+                                                                  heavy_list, counts);
         SPG_LAUNCH_CHECK();
     }
-    exclusive_scan_i64(ctx, prod, pex, m);
-
-    // 3: tiles + heavy rows
-    DBuf<int32_t> flags(ctx, m), heavy(ctx, m), counters(ctx, 2);
-    DBuf<int64_t> tpos(ctx, m + 1);
-    SPG_CUDA(cudaMemsetAsync(counters.get(), 0, 2 * sizeof(int32_t), ctx->stream));
-    {
-        KTime kt(ctx, "tile_plan");
-        k_tile_flags<<<grid_for(ctx, m), 256, 0, ctx->stream>>>(pex, a->rowptr, m, flags, heavy, counters);
-        SPG_LAUNCH_CHECK();
-    }
-    {
-        size_t tmp = 0;
-        SPG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flags.get(), tpos.get(), m, ctx->stream));
-        DBuf<unsigned char> t(ctx, tmp);
-        SPG_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tmp, flags.get(), tpos.get(), m, ctx->stream));
-    }
-    // tpos[m] = number of tiles = tpos[m-1] + flags[m-1]
-    int64_t host[4];
-    {
-        int32_t hflag = 0, hheavy = 0;
-        SPG_CUDA(cudaMemcpyAsync(&host[0], tpos.get() + m - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
-        SPG_CUDA(cudaMemcpyAsync(&hflag, flags.get() + m - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
-        SPG_CUDA(cudaMemcpyAsync(&hheavy, counters.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
-        SPG_CUDA(cudaStreamSynchronize(ctx->stream));
-        host[1] = host[0] + hflag;
-        host[2] = hheavy;
-    }
-    const int64_t ntiles = host[1];
-    const int nheavy = static_cast<int>(host[2]);
-    SPG_CUDA(cudaMemcpyAsync(tpos.get() + m, &host[1], sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
-    DBuf<int32_t> tile_start(ctx, ntiles + 1);
-    k_tile_scatter<<<grid_for(ctx, m), 256, 0, ctx->stream>>>(flags, tpos, m, tile_start);
-    SPG_LAUNCH_CHECK();
+    int32_t hc[2];
+    SPG_CUDA(cudaMemcpyAsync(hc, counts.get(), sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
+    SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+    const int ncta = hc[0], nheavy = hc[1];
 
     // heavy-row workspace plan (host side; heavy rows are few)
     std::vector<int32_t> hrows(nheavy);
     std::vector<int64_t> hp_off(nheavy + 1, 0), he_off(nheavy + 1, 0), hb_off(nheavy + 1, 0);
     if (nheavy) {
-        SPG_CUDA(cudaMemcpyAsync(hrows.data(), heavy.get(), nheavy * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
         DBuf<int64_t> info(ctx, 2 * int64_t(nheavy));
-        k_heavy_info<<<grid_for(ctx, nheavy), 256, 0, ctx->stream>>>(heavy, nheavy, prod, a->rowptr, info);
+        k_heavy_info<<<grid_for(ctx, nheavy), 256, 0, ctx->stream>>>(heavy_list, nheavy, prod, a->rowptr, info);
         SPG_LAUNCH_CHECK();
         std::vector<int64_t> hinfo(2 * size_t(nheavy));
         SPG_CUDA(cudaMemcpyAsync(hinfo.data(), info.get(), hinfo.size() * sizeof(int64_t), cudaMemcpyDeviceToHost,
                                  ctx->stream));
         SPG_CUDA(cudaStreamSynchronize(ctx->stream));
-        std::vector<int64_t> hprod(nheavy), hnent(nheavy);
         for (int h = 0; h < nheavy; ++h) {
-            hprod[h] = hinfo[2 * h];
-            hnent[h] = hinfo[2 * h + 1];
-        }
-        for (int h = 0; h < nheavy; ++h) {
-            hp_off[h + 1] = hp_off[h] + hprod[h];
-            he_off[h + 1] = he_off[h] + hnent[h] + 1;
-            const int64_t nb = (hprod[h] + BUCKET_LOAD - 1) / BUCKET_LOAD;
-            hb_off[h + 1] = hb_off[h] + nb + 1;
+            hp_off[h + 1] = hp_off[h] + hinfo[2 * h];
+            he_off[h + 1] = he_off[h] + hinfo[2 * h + 1] + 1;
+            hb_off[h + 1] = hb_off[h] + (hinfo[2 * h] + BUCKET_LOAD - 1) / BUCKET_LOAD + 1;
         }
     }
-    DBuf<int32_t> d_hrows(ctx, nheavy);
     DBuf<int64_t> d_hp(ctx, nheavy + 1), d_he(ctx, nheavy + 1), d_hb(ctx, nheavy + 1);
     HeavyWs hws{};
     DBuf<int64_t> w_epre(ctx, he_off[nheavy]);
@@ -537,57 +776,68 @@ spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     DBuf<double> w_val(ctx, hp_off[nheavy]);
     DBuf<int64_t> w_boff(ctx, hb_off[nheavy]), w_bcnt(ctx, hb_off[nheavy]);
     if (nheavy) {
-        SPG_CUDA(cudaMemcpyAsync(d_hrows.get(), hrows.data(), nheavy * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
         SPG_CUDA(cudaMemcpyAsync(d_hp.get(), hp_off.data(), (nheavy + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
         SPG_CUDA(cudaMemcpyAsync(d_he.get(), he_off.data(), (nheavy + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
         SPG_CUDA(cudaMemcpyAsync(d_hb.get(), hb_off.data(), (nheavy + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
         hws = HeavyWs{w_epre, w_col, w_val, w_bkt, w_perm, w_boff, w_bcnt};
     }
 
-    const size_t smem = sizeof(TileSmem);
+    const size_t cta_smem = sizeof(CtaSmem);
+    const size_t warp_smem = sizeof(WarpSlice) * WPB;
     if (!ctx->tile_attr_set) {
-        SPG_CUDA(cudaFuncSetAttribute(k_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        SPG_CUDA(cudaFuncSetAttribute(k_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        SPG_CUDA(cudaFuncSetAttribute(k_cta_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cta_smem));
+        SPG_CUDA(cudaFuncSetAttribute(k_cta_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cta_smem));
+        SPG_CUDA(cudaFuncSetAttribute(k_warp_numeric<WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_smem));
         ctx->tile_attr_set = true;
     }
-    int occ = 1;
-    SPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile<true>, NT, smem));
-    const int tgrid = static_cast<int>(std::min<int64_t>(ntiles, int64_t(ctx->num_sms) * std::max(occ, 1) * 8));
+    int occ_w = 1, occ_s = 1;
+    SPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_w, k_warp_numeric<WPB>, WPB * 32, warp_smem));
+    SPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_warp_symbolic<WPB>, WPB * 32, 0));
+    const int64_t wblocks = (m + WPB - 1) / WPB;
+    const int gw = static_cast<int>(std::min<int64_t>(wblocks, int64_t(ctx->num_sms) * std::max(occ_w, 1)));
+    const int gs = static_cast<int>(std::min<int64_t>(wblocks, int64_t(ctx->num_sms) * std::max(occ_s, 1)));
+    const int gc = std::max(1, std::min(ncta, ctx->num_sms * 2));
 
-    // 4: symbolic
+    // 2: symbolic — exact nnz per row
     DBuf<int64_t> rnnz(ctx, m + 1);
     SPG_CUDA(cudaMemsetAsync(rnnz.get(), 0, (m + 1) * sizeof(int64_t), ctx->stream));
     {
         KTime kt(ctx, "spgemm_symbolic");
-        if (ntiles > 0)
-            k_tile<false><<<tgrid, NT, smem, ctx->stream>>>(a->rowptr, a->colind, a->values, b->rowptr, b->colind,
-                                                             b->values, pex, tile_start, static_cast<int>(ntiles),
-                                                             rnnz, nullptr, nullptr, nullptr);
+        k_warp_symbolic<WPB><<<gs, WPB * 32, 0, ctx->stream>>>(a->rowptr, a->colind, b->rowptr, b->colind, m, rnnz);
+        SPG_LAUNCH_CHECK();
+        if (ncta)
+            k_cta_rows<false><<<gc, NT, cta_smem, ctx->stream>>>(a->rowptr, a->colind, a->values, b->rowptr, b->colind,
+                                                                 b->values, prod, cta_list, counts, rnnz, nullptr,
+                                                                 nullptr, nullptr);
         SPG_LAUNCH_CHECK();
         if (nheavy)
             k_heavy<false><<<nheavy, NT, 0, ctx->stream>>>(a->rowptr, a->colind, a->values, b->rowptr, b->colind,
-                                                           b->values, d_hrows, d_hp, d_he, d_hb, hws, rnnz, nullptr,
+                                                           b->values, heavy_list, d_hp, d_he, d_hb, hws, rnnz, nullptr,
                                                            nullptr, nullptr);
         SPG_LAUNCH_CHECK();
     }
-    // 5: rowptr of C
+    // 3: rowptr of C
     spg_csr* c = new_csr(ctx, m, n, -1);
     exclusive_scan_i64(ctx, rnnz, c->rowptr, m);
     c->nnz = read_scalar(ctx, c->rowptr + m);
     c->colind = dalloc<int32_t>(ctx, c->nnz);
     c->values = dalloc<double>(ctx, c->nnz);
 
-    // 6: numeric
+    // 4: numeric
     {
         KTime kt(ctx, "spgemm_numeric");
-        if (ntiles > 0)
-            k_tile<true><<<tgrid, NT, smem, ctx->stream>>>(a->rowptr, a->colind, a->values, b->rowptr, b->colind,
-                                                            b->values, pex, tile_start, static_cast<int>(ntiles),
-                                                            nullptr, c->rowptr, c->colind, c->values);
+        k_warp_numeric<WPB><<<gw, WPB * 32, warp_smem, ctx->stream>>>(a->rowptr, a->colind, a->values, b->rowptr,
+                                                                       b->colind, b->values, m, cshift, c->rowptr,
+                                                                       c->colind, c->values);
+        SPG_LAUNCH_CHECK();
+        if (ncta)
+            k_cta_rows<true><<<gc, NT, cta_smem, ctx->stream>>>(a->rowptr, a->colind, a->values, b->rowptr, b->colind,
+                                                                b->values, prod, cta_list, counts, nullptr, c->rowptr,
+                                                                c->colind, c->values);
         SPG_LAUNCH_CHECK();
         if (nheavy)
             k_heavy<true><<<nheavy, NT, 0, ctx->stream>>>(a->rowptr, a->colind, a->values, b->rowptr, b->colind,
-                                                          b->values, d_hrows, d_hp, d_he, d_hb, hws, nullptr,
+                                                          b->values, heavy_list, d_hp, d_he, d_hb, hws, nullptr,
                                                           c->rowptr, c->colind, c->values);
         SPG_LAUNCH_CHECK();
     }

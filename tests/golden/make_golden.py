@@ -166,5 +166,5 @@ if __name__ == "__main__":
     if what in ("configs", "all"):
         for k in (1, 4, 5, 2):
             config(k)
-    if what.startswith("config"):
+    if what.startswith("config") and what != "configs":
         config(int(what[6:]))
