@@ -1,5 +1,6 @@
 // C-ABI entry points of libspgb200.so (include/spg/capi.h). Every function
 // catches, records the message in a thread-local buffer and returns a status.
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -92,6 +93,8 @@ spg_status spg_init(int device, spg_ctx** out) {
         ctx->device = device;
         ctx->num_sms = prop.multiProcessorCount;
         ctx->l2_bytes = prop.l2CacheSize;
+        const char* two = std::getenv("SPG_TWO_PASS");
+        ctx->force_two_pass = (two && two[0] == '1') ? 1 : 0;
         SPG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         SPG_CUDA(cudaDeviceGetDefaultMemPool(&ctx->pool, device));
         uint64_t keep = UINT64_MAX;  // keep freed blocks cached in the pool

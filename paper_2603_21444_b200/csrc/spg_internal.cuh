@@ -66,6 +66,7 @@ struct spg_ctx {
     // Pinned host staging for small scalar read-backs.
     int64_t* host_scalars = nullptr;
     bool tile_attr_set = false;
+    int force_two_pass = 0;  // 1: never use the single-pass kernel (tests/benchmarks)
 };
 
 struct spg_csr {

@@ -29,16 +29,32 @@ def gpu_mul(dev, a, b, check=True):
     return dc.download()
 
 
+@pytest.fixture(scope="module")
+def dev2():
+    """A second context forced onto the two-pass (symbolic + numeric) path."""
+    import os
+    os.environ["SPG_TWO_PASS"] = "1"
+    try:
+        d = spg.Device(0)
+    finally:
+        del os.environ["SPG_TWO_PASS"]
+    yield d
+    d.close()
+
+
 @pytest.mark.parametrize("name", spgemm_cases())
-def test_spgemm_golden_bit_exact(dev, name):
-    c = gpu_mul(dev, csr(f"{name}_A"), csr(f"{name}_B"))
-    assert same(c, csr(f"{name}_C"))
+def test_spgemm_golden_bit_exact(dev, dev2, name):
+    for d in (dev, dev2):
+        c = gpu_mul(d, csr(f"{name}_A"), csr(f"{name}_B"))
+        assert same(c, csr(f"{name}_C"))
 
 
 @pytest.mark.parametrize("n,d,seed", [(2000, 0.004, 1), (3000, 0.01, 2), (64, 0.5, 3), (1, 1.0, 1), (500, 0.2, 4)])
-def test_spgemm_random_vs_oracle(dev, n, d, seed):
+def test_spgemm_random_vs_oracle(dev, dev2, n, d, seed):
     a, b = O.port_gen_erdos_renyi(n, d, seed), O.port_gen_erdos_renyi(n, d, seed + 7)
-    assert same(gpu_mul(dev, a, b), O.port_spgemm(a, b))
+    ref = O.port_spgemm(a, b)
+    assert same(gpu_mul(dev, a, b), ref)
+    assert same(gpu_mul(dev2, a, b), ref)
 
 
 def test_config1_full_parity(dev):
@@ -72,7 +88,7 @@ def test_edge_cases(dev):
     assert e.value.kind == "DimensionError"
 
 
-def test_heavy_and_skewed_rows(dev):
+def test_heavy_and_skewed_rows(dev, dev2):
     # a row with many entries (heavy by entries), a hub row (heavy by products),
     # clustered columns (banded) and hub columns (many duplicates per column)
     n = 3000
@@ -87,9 +103,13 @@ def test_heavy_and_skewed_rows(dev):
     a = O.ref_from_triplets(n, n, rows, cols, vals) if O.ref_available() else None
     if a is None:
         pytest.skip("needs oracle/_ref for from_triplets")
-    assert same(gpu_mul(dev, a, a), O.port_spgemm(a, a))
+    ref = O.port_spgemm(a, a)
+    assert same(gpu_mul(dev, a, a), ref)
+    assert same(gpu_mul(dev2, a, a), ref)
     r = spg.gen_rmat(12, 16, 1, 2)
-    assert same(gpu_mul(dev, r, r), O.port_spgemm(r, r))
+    ref = O.port_spgemm(r, r)
+    assert same(gpu_mul(dev, r, r), ref)
+    assert same(gpu_mul(dev2, r, r), ref)
 
 
 def test_rectangular_and_transpose(dev):
