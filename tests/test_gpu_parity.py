@@ -31,13 +31,13 @@ def gpu_mul(dev, a, b, check=True):
 
 @pytest.fixture(scope="module")
 def dev2():
-    """A second context forced onto the two-pass (symbolic + numeric) path."""
+    """A second context on the single-pass (decoupled look-back) path."""
     import os
-    os.environ["SPG_TWO_PASS"] = "1"
+    os.environ["SPG_FUSED"] = "1"
     try:
         d = spg.Device(0)
     finally:
-        del os.environ["SPG_TWO_PASS"]
+        del os.environ["SPG_FUSED"]
     yield d
     d.close()
 
