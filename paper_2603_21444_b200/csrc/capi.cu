@@ -93,10 +93,8 @@ spg_status spg_init(int device, spg_ctx** out) {
         ctx->device = device;
         ctx->num_sms = prop.multiProcessorCount;
         ctx->l2_bytes = prop.l2CacheSize;
-        // The two-pass (symbolic + numeric) multiply is the default; the
-        // single-pass look-back kernel is opt-in (SPG_FUSED=1) until it wins.
-        const char* fused = std::getenv("SPG_FUSED");
-        ctx->force_two_pass = (fused && fused[0] == '1') ? 0 : 1;
+        const char* tp = std::getenv("SPG_TWO_PASS");
+        ctx->two_pass = (tp && tp[0] == '1') ? 1 : 0;
         SPG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         SPG_CUDA(cudaDeviceGetDefaultMemPool(&ctx->pool, device));
         uint64_t keep = UINT64_MAX;  // keep freed blocks cached in the pool

@@ -66,7 +66,7 @@ struct spg_ctx {
     // Pinned host staging for small scalar read-backs.
     int64_t* host_scalars = nullptr;
     bool tile_attr_set = false;
-    int force_two_pass = 0;  // 1: never use the single-pass kernel (tests/benchmarks)
+    int two_pass = 0;  // 1: symbolic + numeric warp kernels instead of the single-pass tiles (SPG_TWO_PASS=1)
 };
 
 struct spg_csr {

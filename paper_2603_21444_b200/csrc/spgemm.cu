@@ -224,8 +224,10 @@ struct RowPipe {
     }
 };
 
-// Entry of product x = 32*j + lane: t0 = entry covering 32*j (ballot), plus the
-// entries that start inside the chunk before x (one OR-reduction of start bits).
+// Entry of product x = 32*j + lane (the row's entries with nonempty B rows sit
+// on lanes 0..mn-1 with ascending exclusive product prefix `pre`, INT_MAX past
+// mn): the entry covering position 32j (one ballot) plus the entries that start
+// inside the chunk at or before x (one OR-reduction of start bits).
 __device__ __forceinline__ int chunk_entry(int pre, int j, int lane) {
     const int c0 = 32 * j;
     const int t0 = __popc(__ballot_sync(0xffffffffu, pre <= c0)) - 1;
@@ -234,61 +236,35 @@ __device__ __forceinline__ int chunk_entry(int pre, int j, int lane) {
     return t0 + __popc(sm & ((2u << lane) - 1u));
 }
 
-// Per-warp smem slice of the numeric kernel for rows of ≤ 32*NJ products:
-// products in bucket order and the 2p bucket counters / offsets.
-template <int NJ>
-struct WarpSliceT {
-    static constexpr int P = 32 * NJ;
-    int32_t col[P];
-    double val[P];
-    int64_t e_base[32];  // per entry: B position of product x is e_base[t] + x
-    double e_av[32];
-    uint16_t x[P];
-    uint8_t e_of[P];     // entry of product x
-    int32_t off[2 * P + 1];
-    int32_t big[P / 3 + 1];  // starts of buckets holding >= 3 products
-    int32_t nbig;
-};
-
-// Entry tables of a row in the warp's smem: lane t < mn owns entry t and fills
-// e_of over its product range. Replaces per-product warp collectives.
-template <bool VALS>
-__device__ __forceinline__ void fill_entries(const RowEntries& re, int64_t* e_base, double* e_av, uint8_t* e_of,
-                                             int lane) {
-    const int hi = __shfl_down_sync(0xffffffffu, re.pre, 1);
-    if (re.pre != INT_MAX) {
-        e_base[lane] = re.base;
-        if (VALS) e_av[lane] = re.av;
-        const int end = (lane == 31 || hi == INT_MAX) ? re.p : hi;
-        for (int x = re.pre; x < end; ++x) e_of[x] = static_cast<uint8_t>(lane);
-    }
-    __syncwarp();
-}
-using WarpSlice = WarpSliceT<WARP_NJ>;
-
 // Row classes of the warp kernels: NJ = 8 for products in [1, 256], NJ = 16
 // for (256, 512] (separate kernels so the small class runs at higher occupancy).
-template <int NJ>
-__device__ __forceinline__ bool in_class(int64_t p, int ne) {
-    return ne <= 32 && p > (NJ == 8 ? 0 : 256) && p <= 32 * NJ;
-}
+// Bucket counters: W 32-bit words, two 16-bit counters each (nb = 2W buckets).
+// SPG_NB_SHIFT = 1: ~0.5 products per bucket; 0: ~1.
+#ifndef SPG_NB_SHIFT
+#define SPG_NB_SHIFT 1
+#endif
+__device__ __forceinline__ int count_words(int p) { return SPG_NB_SHIFT ? p : (p + 1) >> 1; }
 
 // --------------------------------------------------------- warp symbolic
-// Distinct columns per row via an open-addressing set in the warp's smem.
+// Distinct columns per row: every product's column goes into an open-addressing
+// set (atomicCAS) in the warp's smem slice; gathers are coalesced across lanes.
+template <int NJ>
+struct __align__(16) WarpSymSmem {
+    int64_t e_base[32];     // per entry: B position of product x is e_base[t] + x
+    int32_t tab[64 * NJ];   // 2^lg >= 2p slots, -1 = empty
+};
+
 template <int WPB, int NJ>
-__global__ void __launch_bounds__(WPB * 32, 4) k_warp_symbolic(const int64_t* __restrict__ arp,
+__global__ void __launch_bounds__(WPB * 32) k_warp_symbolic(const int64_t* __restrict__ arp,
                                                             const int32_t* __restrict__ acol,
                                                             const int64_t* __restrict__ brp,
                                                             const int32_t* __restrict__ bcol,
                                                             const int32_t* __restrict__ list,
                                                             const int32_t* __restrict__ count,
                                                             int64_t* __restrict__ row_nnz) {
-    constexpr int T = 2 * 32 * NJ;
-    __shared__ int32_t table[WPB][T];
-    __shared__ int64_t s_base[WPB][32];
-    __shared__ uint8_t s_of[WPB][32 * NJ];
+    __shared__ WarpSymSmem<NJ> smem[WPB];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    int32_t* tab = table[w];
+    WarpSymSmem<NJ>& S = smem[w];
     const int64_t gw = blockIdx.x * int64_t(WPB) + w, nw = int64_t(gridDim.x) * WPB;
     RowPipe<false> pipe{arp, acol, nullptr, brp, list, *count, nw};
     int32_t i;
@@ -296,16 +272,21 @@ __global__ void __launch_bounds__(WPB * 32, 4) k_warp_symbolic(const int64_t* __
     for (int64_t t = gw; t < pipe.n; t += nw) {
         const RowEntries re = make_row(cur, lane);
         const int p = re.p;
-        const int lg = max(6, 32 - __clz(2 * p - 1));  // 2^lg >= 2p
+        const int lg = max(5, 32 - __clz(2 * p - 1));  // 2^lg >= 2p
         const int TT = 1 << lg;
-        for (int q = lane; q < TT; q += 32) tab[q] = -1;
+        if (re.pre != INT_MAX) S.e_base[lane] = re.base;
+        int4* t4 = reinterpret_cast<int4*>(S.tab);
+        for (int q = lane; q < (TT >> 2); q += 32) t4[q] = make_int4(-1, -1, -1, -1);
         __syncwarp();
-        fill_entries<false>(re, s_base[w], nullptr, s_of[w], lane);
         int32_t cols[NJ];
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
-            const int x = 32 * j + lane;
-            cols[j] = x < p ? __ldg(bcol + s_base[w][s_of[w][x]] + x) : -1;
+            cols[j] = -1;
+            if (32 * j < p) {  // warp-uniform
+                const int te = chunk_entry(re.pre, j, lane);
+                const int x = 32 * j + lane;
+                if (x < p) cols[j] = __ldg(bcol + S.e_base[te] + x);
+            }
         }
         const RowFetch nxt = pipe.spans(lane);
         int fresh = 0;
@@ -314,15 +295,13 @@ __global__ void __launch_bounds__(WPB * 32, 4) k_warp_symbolic(const int64_t* __
             if (cols[j] < 0) continue;
             uint32_t h = (static_cast<uint32_t>(cols[j]) * 0x9E3779B1u) >> (32 - lg);
             while (true) {
-                const int32_t old = atomicCAS(&tab[h], -1, cols[j]);
+                const int32_t old = atomicCAS(&S.tab[h], -1, cols[j]);
                 if (old == -1) { ++fresh; break; }
                 if (old == cols[j]) break;
                 h = (h + 1) & (TT - 1);
             }
         }
-        __syncwarp();
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) fresh += __shfl_xor_sync(0xffffffffu, fresh, o);
+        fresh = warp_reduce_sum(fresh);
         if (lane == 0) row_nnz[i] = fresh;
         const int32_t inext = pipe.i1;
         pipe.advance(t + nw, lane);
@@ -333,136 +312,137 @@ __global__ void __launch_bounds__(WPB * 32, 4) k_warp_symbolic(const int64_t* __
 }
 
 // ---------------------------------------------------------- warp numeric
-// Products are gathered into registers (x = 32j + lane, ascending k within the
-// row), counted into 2p column buckets, and scattered once into the warp's smem
-// slice in bucket order. Singleton buckets are final, pairs are ordered by one
-// compare in registers, and buckets of ≥ 3 are insertion-sorted by (col, x)
-// from a short list: the slice then holds the row sorted by column. Runs of
-// equal columns (duplicates; rare for ER) are summed in x order (= ascending
-// k, separate mul and add) and compacted in place, so values are bit-identical
-// to the reference. Returns nnz; the row is S.col[0..nnz), S.val[0..nnz).
-// Warp-collective operations are never under a data-dependent branch.
+// Per-warp smem slice for rows of <= 32*NJ products.
 template <int NJ>
-__device__ __forceinline__ int warp_row_sorted(WarpSliceT<NJ>& S, const RowEntries& re,
-                                               const int32_t* __restrict__ bcol, const double* __restrict__ bval,
-                                               int cshift, int lane) {
-    const int p = re.p;
-    const int nb = 2 * p;  // ~0.5 products per bucket
-    for (int q = lane; q <= nb; q += 32) S.off[q] = 0;
+struct __align__(16) WarpRowSmem {
+    static constexpr int P = 32 * NJ;
+    double val[P];          // the row of C in column order (values); product ids while ordering
+    int64_t e_base[32];     // per entry: B position of product x is e_base[t] + x
+    double e_av[32];        // per entry: A value
+    int32_t col[P];         // the row of C in column order (columns)
+    uint32_t cnt[P + 4];    // bucket counters (2 x 16 bit per word), then their prefixes
+};
 
-    fill_entries<true>(re, S.e_base, S.e_av, S.e_of, lane);
-    // expand: every gather issued before any is consumed
+// One row of C into S.col/S.val (sorted by column, duplicates combined).
+// Products live in registers (x = 32j + lane, ascending k within the row); each
+// goes to one of nb column buckets (a monotone map of the column), a warp scan
+// of the packed 16-bit counters gives bucket offsets, products alone in their
+// bucket are placed directly, and products sharing a bucket are ranked by
+// (column, x) against the few others. Equal columns (duplicates) are summed in
+// x order = ascending k with a separate multiply and add, so values are
+// bit-identical to the reference's acc[j] += av*bv (csr.cpp:149-154).
+// Returns the row's nnz. Warp collectives are never under divergent control.
+template <int NJ>
+__device__ __forceinline__ int warp_row_numeric(WarpRowSmem<NJ>& S, const RowEntries& re,
+                                                const int32_t* __restrict__ bcol, const double* __restrict__ bval,
+                                                int cshift, int lane) {
+    const int p = re.p;
+    const int W = count_words(p);
+    const int nb = 2 * W;
+    if (re.pre != INT_MAX) {
+        S.e_base[lane] = re.base;
+        S.e_av[lane] = re.av;
+    }
+    for (int q = lane; q <= W; q += 32) S.cnt[q] = 0u;
+    __syncwarp();
+    // expand: all gathers of the row issued before any is consumed
     int32_t col[NJ];
     double val[NJ];
-    int aux[NJ];  // entry index, then the bucket's first position, then the target
+    int aux[NJ];  // entry, then the position in the row
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
-        const int x = 32 * j + lane;
         col[j] = 0;
         val[j] = 0.0;
-        aux[j] = 0;
-        if (x < p) {
-            const int t = S.e_of[x];
-            const int64_t u = S.e_base[t] + x;
-            aux[j] = t;
-            col[j] = __ldg(bcol + u);
-            val[j] = __ldg(bval + u);
-        }
-    }
-    int slot[NJ];
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-        slot[j] = -1;
-        if (32 * j + lane < p) {
-            val[j] = dmul(S.e_av[aux[j]], val[j]);
-            slot[j] = atomicAdd(&S.off[bucket_of(col[j], cshift, nb)], 1);
-        }
-    }
-    __syncwarp();
-    // exclusive scan of the nb counts (contiguous block per lane); off[nb] = p
-    {
-        const int per = (nb + 1 + 31) >> 5;
-        const int b0 = lane * per;
-        int s = 0;
-        for (int q = 0; q < per; ++q) s += (b0 + q < nb) ? S.off[b0 + q] : 0;
-        int inc = s;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
-        }
-        int pre = inc - s;
-        __syncwarp();
-        for (int q = 0; q < per; ++q) {
-            const int b = b0 + q;
-            if (b <= nb) {
-                const int c = b < nb ? S.off[b] : 0;
-                S.off[b] = pre;
-                pre += c;
+        aux[j] = -1;
+        if (32 * j < p) {  // warp-uniform
+            const int te = chunk_entry(re.pre, j, lane);
+            const int x = 32 * j + lane;
+            if (x < p) {
+                const int64_t u = S.e_base[te] + x;
+                aux[j] = te;
+                col[j] = __ldg(bcol + u);
+                val[j] = __ldg(bval + u);
             }
         }
-        if (lane == 0) S.nbig = 0;
     }
-    __syncwarp();
-    // scatter into bucket order; remember each product's bucket start
+    // multiply (0 + av*bv: the reference's first accumulation) and count
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
-        if (slot[j] >= 0) {
-            const int lo = S.off[bucket_of(col[j], cshift, nb)];
-            aux[j] = lo;
-            S.col[lo + slot[j]] = col[j];
-            S.val[lo + slot[j]] = val[j];
-            S.x[lo + slot[j]] = static_cast<uint16_t>(32 * j + lane);
+        if (aux[j] >= 0) {
+            val[j] = dadd(0.0, dmul(S.e_av[aux[j]], val[j]));
+            const int b = bucket_of(col[j], cshift, nb);
+            const int sh = (b & 1) << 4;
+            aux[j] = static_cast<int>((atomicAdd(&S.cnt[b >> 1], 1u << sh) >> sh) & 0xffffu);
+        }
+    }
+    __syncwarp();
+    // exclusive scan of the packed counters: lane owns an odd-strided block of
+    // words (conflict-free); word k becomes (prefix(2k), prefix(2k+1))
+    {
+        const int per = ((W + 31) >> 5) | 1;
+        const int w0 = lane * per;
+        uint32_t sum = 0;
+        for (int q = 0; q < per; ++q)
+            if (w0 + q < W) sum += S.cnt[w0 + q];
+        const int tot = static_cast<int>((sum & 0xffffu) + (sum >> 16));
+        uint32_t pre = static_cast<uint32_t>(warp_inclusive_scan(tot) - tot);
+        for (int q = 0; q < per; ++q) {
+            if (w0 + q < W) {
+                const uint32_t wd = S.cnt[w0 + q];
+                S.cnt[w0 + q] = pre * 0x10001u + (wd << 16);
+                pre += (wd + (wd << 16)) >> 16;
+            }
+        }
+        if (lane == 0) S.cnt[W] = static_cast<uint32_t>(p);  // end of the last bucket
+    }
+    __syncwarp();
+    // place: a product alone in its bucket is final; shared buckets collect
+    // (column, x) for ranking (x parked in the value array)
+    uint16_t* xs = reinterpret_cast<uint16_t*>(S.val);
+    unsigned shared = 0;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        if (aux[j] >= 0) {
+            const int b = bucket_of(col[j], cshift, nb);
+            const uint32_t r = __funnelshift_r(S.cnt[b >> 1], S.cnt[(b >> 1) + 1], (b & 1) << 4);
+            const int st = static_cast<int>(r & 0xffffu);
+            const int pos = st + aux[j];
+            S.col[pos] = col[j];
+            if ((r >> 16) - st > 1) {
+                xs[pos] = static_cast<uint16_t>(32 * j + lane);
+                shared |= 1u << j;
+            }
+            aux[j] = pos;
         }
     }
     __syncwarp();
     bool dup = false;
+    if (shared) {
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-        int dst = -1;
-        if (slot[j] >= 0) {
-            const int lo = aux[j];
-            const int sz = S.off[bucket_of(col[j], cshift, nb) + 1] - lo;
-            if (sz == 2) {
-                const int other = lo + 1 - slot[j];
-                const int32_t pc = S.col[other];
-                const bool eq = pc == col[j];
-                dup |= eq;
-                const int r = (pc < col[j] || (eq && S.x[other] < 32 * j + lane)) ? 1 : 0;
-                if (r != slot[j]) dst = lo + r;
-            } else if (sz > 2 && slot[j] == 0) {
-                S.big[atomicAdd(&S.nbig, 1)] = lo;
+        for (int j = 0; j < NJ; ++j) {
+            if ((shared >> j) & 1u) {
+                const int b = bucket_of(col[j], cshift, nb);
+                const uint32_t r = __funnelshift_r(S.cnt[b >> 1], S.cnt[(b >> 1) + 1], (b & 1) << 4);
+                const int st = static_cast<int>(r & 0xffffu), en = static_cast<int>(r >> 16);
+                const int x = 32 * j + lane;
+                int rank = 0;
+                for (int q = st; q < en; ++q) {
+                    const int32_t cq = S.col[q];
+                    const int xq = xs[q];
+                    rank += (cq < col[j]) || (cq == col[j] && xq < x);
+                    dup |= (cq == col[j]) && (xq != x);
+                }
+                aux[j] = st + rank;
             }
         }
-        aux[j] = dst;
     }
     __syncwarp();
 #pragma unroll
-    for (int j = 0; j < NJ; ++j)
+    for (int j = 0; j < NJ; ++j) {
         if (aux[j] >= 0) {
-            S.col[aux[j]] = col[j];
+            if ((shared >> j) & 1u) S.col[aux[j]] = col[j];
             S.val[aux[j]] = val[j];
         }
-    const int nbig = S.nbig;
-    for (int k = lane; k < nbig; k += 32) {
-        const int lo = S.big[k];
-        const int hi = S.off[bucket_of(S.col[lo], cshift, nb) + 1];
-        for (int q = lo + 1; q < hi; ++q) {
-            const int32_t cq = S.col[q];
-            const double vq = S.val[q];
-            const uint16_t xq = S.x[q];
-            int r = q - 1;
-            while (r >= lo && (S.col[r] > cq || (S.col[r] == cq && S.x[r] > xq))) {
-                S.col[r + 1] = S.col[r];
-                S.val[r + 1] = S.val[r];
-                S.x[r + 1] = S.x[r];
-                --r;
-            }
-            S.col[r + 1] = cq;
-            S.val[r + 1] = vq;
-            S.x[r + 1] = xq;
-        }
-        for (int q = lo + 1; q < hi; ++q) dup |= S.col[q] == S.col[q - 1];
     }
     __syncwarp();
     if (!__any_sync(0xffffffffu, dup)) return p;
@@ -477,7 +457,7 @@ __device__ __forceinline__ int warp_row_sorted(WarpSliceT<NJ>& S, const RowEntri
         double sum = 0.0;
         if (head) {
             c = S.col[q];
-            sum = dadd(0.0, S.val[q]);
+            sum = S.val[q];
             for (int u = q + 1; u < p && S.col[u] == c; ++u) sum = dadd(sum, S.val[u]);
         }
         __syncwarp();
@@ -493,11 +473,11 @@ __device__ __forceinline__ int warp_row_sorted(WarpSliceT<NJ>& S, const RowEntri
 }
 
 template <int NJ>
-__device__ __forceinline__ void warp_copy_out(const WarpSliceT<NJ>& S, int nnz, int64_t obase,
+__device__ __forceinline__ void warp_copy_out(const WarpRowSmem<NJ>& S, int nnz, int64_t obase,
                                               int32_t* __restrict__ ccol, double* __restrict__ cval, int lane) {
     for (int q = lane; q < nnz; q += 32) {
         ccol[obase + q] = S.col[q];
-        cval[obase + q] = dadd(0.0, S.val[q]);
+        cval[obase + q] = S.val[q];
     }
 }
 
@@ -515,14 +495,14 @@ __global__ void __launch_bounds__(WPB * 32, MINB) k_warp_numeric(const int64_t* 
                                                                  double* __restrict__ cval) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    WarpSliceT<NJ>& S = reinterpret_cast<WarpSliceT<NJ>*>(smem_raw)[w];
+    WarpRowSmem<NJ>& S = reinterpret_cast<WarpRowSmem<NJ>*>(smem_raw)[w];
     const int64_t gw = blockIdx.x * int64_t(WPB) + w, nw = int64_t(gridDim.x) * WPB;
     RowPipe<true> pipe{arp, acol, aval, brp, list, *count, nw};
     int32_t i;
     RowFetch cur = pipe.start(gw, lane, i);
     for (int64_t t = gw; t < pipe.n; t += nw) {
         const RowEntries re = make_row(cur, lane);
-        const int nnz = warp_row_sorted<NJ>(S, re, bcol, bval, cshift, lane);
+        const int nnz = warp_row_numeric<NJ>(S, re, bcol, bval, cshift, lane);
         const RowFetch nxt = pipe.spans(lane);
         warp_copy_out<NJ>(S, nnz, crp[i], ccol, cval, lane);
         const int32_t inext = pipe.i1;
@@ -533,107 +513,6 @@ __global__ void __launch_bounds__(WPB * 32, MINB) k_warp_numeric(const int64_t* 
     }
 }
 
-// ------------------------------------------------------------- fused pass
-// Single pass: warps take rows in order from a global ticket, compute the
-// sorted row into their smem slice, publish its nnz, and find the row's offset
-// in C with a decoupled look-back over the predecessors' status words (a warp
-// only ever waits on rows with smaller tickets, which are already running, so
-// progress is guaranteed). Rows of the CTA / heavy classes were computed
-// beforehand into a side buffer; their warp just publishes and copies.
-// status word: bits 62-63 flag (0 none, 1 aggregate, 2 inclusive), bits 0-61 value.
-constexpr uint64_t ST_AGG = 1ull << 62, ST_INC = 2ull << 62, ST_VAL = (1ull << 62) - 1;
-
-__device__ __forceinline__ uint64_t ld_status(const uint64_t* p) {
-    uint64_t v;
-    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_status(uint64_t* p, uint64_t v) {
-    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// Exclusive prefix of row i's nnz over rows [0, i) (all lanes return it).
-__device__ __forceinline__ int64_t look_back(const uint64_t* status, int64_t i, int lane) {
-    int64_t excl = 0;
-    int64_t j = i - 1;
-    while (j >= 0) {
-        const int64_t idx = j - lane;
-        uint64_t s = idx >= 0 ? ld_status(status + idx) : ST_INC;
-        while (true) {
-            const unsigned inc = __ballot_sync(0xffffffffu, (s >> 62) == 2);
-            const unsigned none = __ballot_sync(0xffffffffu, (s >> 62) == 0);
-            const unsigned upto = inc ? ((inc & (0u - inc)) << 1) - 1u : 0xffffffffu;  // lanes <= first inclusive
-            if (none & upto) {
-                if ((s >> 62) == 0 && idx >= 0) s = ld_status(status + idx);
-                continue;
-            }
-            int64_t v = ((1u << lane) & upto) ? static_cast<int64_t>(s & ST_VAL) : 0;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            excl += v;
-            if (inc) return excl;
-            break;
-        }
-        j -= 32;
-    }
-    return excl;
-}
-
-template <int WPB>
-__global__ void __launch_bounds__(WPB * 32, SPG_WARP_MINB) k_warp_fused(
-    const int64_t* __restrict__ arp, const int32_t* __restrict__ acol, const double* __restrict__ aval,
-    const int64_t* __restrict__ brp, const int32_t* __restrict__ bcol, const double* __restrict__ bval, int64_t m,
-    int cshift, const int64_t* __restrict__ side_off, const int64_t* __restrict__ side_nnz,
-    const int32_t* __restrict__ side_col, const double* __restrict__ side_val, unsigned long long* __restrict__ ticket,
-    uint64_t* __restrict__ status, int64_t* __restrict__ crp, int32_t* __restrict__ ccol, double* __restrict__ cval) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    WarpSlice& S = reinterpret_cast<WarpSlice*>(smem_raw)[w];
-    while (true) {
-        int64_t i = 0;
-        if (lane == 0) i = static_cast<int64_t>(atomicAdd(ticket, 1ull));
-        i = __shfl_sync(0xffffffffu, i, 0);
-        if (i >= m) break;
-        const int64_t e0 = arp[i];
-        const int ne = static_cast<int>(arp[i + 1] - e0);
-        const int64_t so = side_off[i];
-        int64_t nnz = 0;
-        if (so >= 0) {
-            nnz = side_nnz[i];
-        } else if (ne > 0 && ne <= 32) {
-            const RowEntries re = load_row<true>(acol, aval, brp, e0, ne, lane);
-            if (re.p > 0) nnz = warp_row_sorted<WARP_NJ>(S, re, bcol, bval, cshift, lane);
-        }
-        if (lane == 0) st_status(status + i, (i == 0 ? ST_INC : ST_AGG) | static_cast<uint64_t>(nnz));
-        const int64_t excl = i == 0 ? 0 : look_back(status, i, lane);
-        if (lane == 0) {
-            if (i > 0) st_status(status + i, ST_INC | static_cast<uint64_t>(excl + nnz));
-            crp[i + 1] = excl + nnz;
-        }
-        if (so >= 0) {
-            for (int64_t q = lane; q < nnz; q += 32) {
-                ccol[excl + q] = side_col[so + q];
-                cval[excl + q] = side_val[so + q];
-            }
-        } else {
-            warp_copy_out<WARP_NJ>(S, static_cast<int>(nnz), excl, ccol, cval, lane);
-        }
-        __syncwarp();
-    }
-}
-
-// side_off[row] = offset of a CTA/heavy row in the side buffer (products-bounded).
-__global__ void k_side_gather(const int32_t* __restrict__ rows, const int32_t* __restrict__ count,
-                              const int64_t* __restrict__ prod, int64_t* __restrict__ out) {
-    const int n = *count;
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) out[t] = prod[rows[t]];
-}
-
-__global__ void k_side_scatter(const int32_t* __restrict__ rows, const int32_t* __restrict__ count,
-                               const int64_t* __restrict__ off, int64_t* __restrict__ side_off) {
-    const int n = *count;
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) side_off[rows[t]] = off[t];
-}
 
 // ---------------------------------------------------------------- CTA rows
 // One CTA per row (≤ CTA_P products, ≤ CTA_E entries): the same bucketed ESC
@@ -932,6 +811,600 @@ __global__ void k_heavy_info(const int32_t* __restrict__ rows, int n, const int6
 }
 
 
+// ======================================================= single-pass tiles
+// The default local multiply. Rows are cut into TILES of
+// consecutive rows; one CTA multiplies a whole tile in shared memory (a
+// CTA-wide bucketed ESC over all of the tile's products, keyed by
+// (row, column)), finds the tile's offset in C with a decoupled look-back over
+// the tile aggregates, and writes the tile as one contiguous run of C. There is
+// no symbolic pass: every B entry is gathered once. Rows too large for a tile
+// (BIG rows) are multiplied beforehand into a side buffer by the CTA / heavy
+// row kernels and occupy a tile of their own that only copies.
+namespace tile {
+constexpr int NT = 256;                         // threads per CTA
+constexpr int NW = NT / 32;
+constexpr int SMALL_P = 512;                    // a tile row has <= SMALL_P products
+constexpr int SMALL_E = 64;                     // ... and <= SMALL_E entries
+constexpr int ROW_W_MAX = SMALL_P + 4 * SMALL_E + 4;
+#ifndef SPG_TILE_W
+#define SPG_TILE_W 2048
+#endif
+constexpr int TW = SPG_TILE_W;                  // tile window of the row weight prefix
+constexpr int PMAX = TW + ROW_W_MAX;            // bound of products, 4*entries, 4*rows of a tile
+constexpr int EMAX = PMAX / 4;
+constexpr int RMAX = PMAX / 4;
+constexpr int NJ = (PMAX + NT - 1) / NT;        // product slots per thread
+constexpr int EPT = (EMAX + NT - 1) / NT;       // entry slots per thread
+constexpr int HW = PMAX / 32 + 2;               // words of the head bitmap
+constexpr int LMAX = PMAX / 3 + 1;              // shared buckets of >= 3 products
+// espan[e] of an entry of a tile row: B row start (34 bits) | B row length (10)
+// | product offset of the entry in its row (10) | products of the row (10)
+constexpr int SP_BS = 34, SP_LEN = 34, SP_IN = 44, SP_PR = 54;
+constexpr uint64_t SP_BS_MASK = (uint64_t(1) << SP_BS) - 1;
+}  // namespace tile
+
+// Row weight: tiles are runs of small rows within one TW-window of the
+// exclusive prefix of weights, so a tile has < PMAX products, < PMAX/4
+// entries and < PMAX/4 rows.
+__host__ __device__ __forceinline__ int64_t tile_weight(int64_t p, int64_t ne) { return p + 4 * ne + 4; }
+__host__ __device__ __forceinline__ bool tile_small(int64_t p, int64_t ne) {
+    return p <= tile::SMALL_P && ne <= tile::SMALL_E;
+}
+
+// Per row (warp per row, lanes over entries): products(i) = Σ nnz(B_k), the
+// packed entry spans of tile rows (so the tile kernel reads its entries with no
+// dependent B.rowptr load and no row pass), the row weight, and the BIG-row
+// lists: 0 = CTA rows (<= CTA_P products, <= CTA_E entries), 1 = heavy.
+__global__ void k_row_prep(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
+                           const int64_t* __restrict__ brp, int64_t m, int64_t* __restrict__ prod,
+                           int64_t* __restrict__ wt, uint64_t* __restrict__ espan, int32_t* __restrict__ lists,
+                           int32_t* __restrict__ counts) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t i = gw; i < m; i += nw) {
+        const int64_t e0 = arp[i], e1 = arp[i + 1];
+        int64_t p = 0;
+        int64_t bsv[2] = {0, 0};
+        int lenv[2] = {0, 0}, inv[2] = {0, 0};
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {  // the first 64 entries (all of a tile row's)
+            const int64_t e = e0 + 32 * c + lane;
+            int64_t len = 0;
+            if (e < e1) {
+                const int32_t k = __ldg(acol + e);
+                bsv[c] = __ldg(brp + k);
+                len = __ldg(brp + k + 1) - bsv[c];
+            }
+            const int64_t inc = warp_inclusive_scan(len);
+            inv[c] = static_cast<int>(min(p + inc - len, int64_t(1023)));
+            lenv[c] = static_cast<int>(min(len, int64_t(1023)));
+            p += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        for (int64_t eb = e0 + 64; eb < e1; eb += 32) {  // BIG rows only (> 64 entries)
+            const int64_t e = eb + lane;
+            int64_t len = 0;
+            if (e < e1) {
+                const int32_t k = __ldg(acol + e);
+                len = __ldg(brp + k + 1) - __ldg(brp + k);
+            }
+            p += warp_reduce_sum(len);
+        }
+        const int64_t ne = e1 - e0;
+        const bool small = tile_small(p, ne);
+        if (small) {
+            const uint64_t pr = static_cast<uint64_t>(p);
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int64_t e = e0 + 32 * c + lane;
+                if (e < e1)
+                    espan[e] = (static_cast<uint64_t>(bsv[c]) & tile::SP_BS_MASK) |
+                               (static_cast<uint64_t>(lenv[c]) << tile::SP_LEN) |
+                               (static_cast<uint64_t>(inv[c]) << tile::SP_IN) | (pr << tile::SP_PR);
+            }
+        }
+        if (lane == 0) {
+            prod[i] = p;
+            wt[i] = small ? tile_weight(p, ne) : 0;
+            if (!small) {
+                const int c = (ne <= CTA_E && p <= CTA_P) ? 0 : 1;
+                lists[c * m + atomicAdd(counts + c, 1)] = static_cast<int32_t>(i);
+            }
+        }
+    }
+}
+
+// Tile starts: row i starts a tile if it is BIG, follows a BIG row, or its
+// weight prefix enters a new TW-window.
+__global__ void k_tile_flags(const int64_t* __restrict__ wpre, const int64_t* __restrict__ prod,
+                             const int64_t* __restrict__ arp, int64_t m, int64_t* __restrict__ flag) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
+        const bool big = !tile_small(prod[i], arp[i + 1] - arp[i]);
+        int f = 1;
+        if (i > 0 && !big) {
+            const bool prev_big = !tile_small(prod[i - 1], arp[i] - arp[i - 1]);
+            f = prev_big || (wpre[i] / tile::TW != wpre[i - 1] / tile::TW);
+        }
+        flag[i] = f;
+    }
+}
+
+// Compacts the tile starts: tr[t] = first row | BIG flag (bit 62), te[t] = its
+// first entry; tr[ntiles] = m, te[ntiles] = nnz(A).
+__global__ void k_tile_scatter(const int64_t* __restrict__ flag, const int64_t* __restrict__ fpos,
+                               const int64_t* __restrict__ prod, const int64_t* __restrict__ arp, int64_t m,
+                               int64_t* __restrict__ tr, int64_t* __restrict__ te) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i <= m; i += int64_t(gridDim.x) * blockDim.x) {
+        if (i == m) {
+            const int64_t nt = fpos[m];
+            tr[nt] = m;
+            te[nt] = arp[m];
+        } else if (flag[i]) {
+            const bool big = !tile_small(prod[i], arp[i + 1] - arp[i]);
+            tr[fpos[i]] = i | (big ? (int64_t(1) << 62) : 0);
+            te[fpos[i]] = arp[i];
+        }
+    }
+}
+
+// side_off[row] / side_nnz[row] of the BIG rows from their list order.
+__global__ void k_side_gather(const int32_t* __restrict__ rows, int n, const int64_t* __restrict__ rnnz,
+                              int64_t* __restrict__ out) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) out[t] = rnnz[rows[t]];
+}
+__global__ void k_side_scatter(const int32_t* __restrict__ rows, int n, const int64_t* __restrict__ off,
+                               int64_t* __restrict__ side_off) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) side_off[rows[t]] = off[t];
+}
+
+// Decoupled look-back status word: bits 62-63 flag (0 none, 1 aggregate,
+// 2 inclusive prefix), bits 0-61 value.
+constexpr uint64_t ST_AGG = 1ull << 62, ST_INC = 2ull << 62, ST_VAL = (1ull << 62) - 1;
+
+__device__ __forceinline__ uint64_t ld_status(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_status(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Exclusive block scan with one barrier: warp totals go to ws (NW slots); the
+// caller guarantees a barrier between two uses of the same ws.
+template <typename T>
+__device__ __forceinline__ T tile_scan(T v, T* total, T* ws) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const T inc = warp_inclusive_scan(v);
+    if (lane == 31) ws[wid] = inc;
+    __syncthreads();
+    T before = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < tile::NW; ++w) {
+        const T t = ws[w];
+        before += w < wid ? t : T(0);
+        tot += t;
+    }
+    *total = tot;
+    return before + inc - v;
+}
+
+struct __align__(16) TileEnt {
+    int64_t base;  // B position of tile product x is base + x
+    double av;     // A value
+};
+
+struct __align__(16) TileSmem {
+    double val[tile::PMAX];        // staging: the tile's C entries (values)
+    TileEnt ent[tile::EMAX];
+    int32_t col[tile::PMAX];       // staging: columns
+    uint32_t cnt[tile::PMAX + 2];  // 2 x 16-bit bucket counters per word, then prefixes
+    uint32_t ebin[tile::EMAX];     // per entry: row bucket base (lo 16) | row bucket count (hi 16)
+    int32_t epre[tile::EMAX + 1];  // product prefix of the tile's entries
+    int32_t re[tile::RMAX + 1];    // first entry of each row (relative to the tile)
+    int32_t rend[tile::RMAX];      // end of each row in the (compacted) staging
+    uint32_t list[tile::LMAX];     // shared buckets of >= 3 products: start | end << 16
+    uint32_t hbm[tile::HW];        // duplicate path: head bitmap
+    int32_t hpre[tile::HW];        //   and its word prefix
+    uint16_t xs[tile::PMAX];       // product id of a staged entry of a shared bucket
+    uint16_t eof[tile::PMAX];      // entry of each product
+    int32_t ws[4][tile::NW];       // scan workspaces (rotated)
+    int64_t lbs[tile::NW];         // look-back: per-warp sums
+    int32_t lbi[tile::NW];         //   and "found an inclusive prefix"
+    int64_t ticket;                // next tile of this CTA
+    int32_t nlist;
+};
+
+// Tile descriptor (uniform across the CTA).
+struct TileDesc {
+    int64_t k, r0, e0;
+    int R, E, ptile;
+    bool big;
+};
+
+// Number of heads (distinct (row, column) runs) before staging position q.
+__device__ __forceinline__ int head_prefix(const TileSmem& S, int q) {
+    return S.hpre[q >> 5] + __popc(S.hbm[q >> 5] & ((1u << (q & 31)) - 1u));
+}
+
+// Contiguous smem -> global copy of n staged entries to C[base, base+n) with
+// 16-byte stores in the aligned middle.
+__device__ __forceinline__ void tile_copy_out(const TileSmem& S, int n, int64_t base, int32_t* __restrict__ ccol,
+                                              double* __restrict__ cval, int tid) {
+    {
+        const int head = min(n, static_cast<int>((4 - (base & 3)) & 3));
+        const int nv = (n - head) >> 2;
+        if (tid < head) ccol[base + tid] = S.col[tid];
+        int4* dst = reinterpret_cast<int4*>(ccol + base + head);
+        for (int v = tid; v < nv; v += tile::NT) {
+            const int q = head + 4 * v;
+            dst[v] = make_int4(S.col[q], S.col[q + 1], S.col[q + 2], S.col[q + 3]);
+        }
+        for (int q = head + 4 * nv + tid; q < n; q += tile::NT) ccol[base + q] = S.col[q];
+    }
+    {
+        const int head = min(n, static_cast<int>(base & 1));
+        const int nv = (n - head) >> 1;
+        if (tid < head) cval[base + tid] = S.val[tid];
+        double2* dst = reinterpret_cast<double2*>(cval + base + head);
+        for (int v = tid; v < nv; v += tile::NT) {
+            const int q = head + 2 * v;
+            dst[v] = make_double2(S.val[q], S.val[q + 1]);
+        }
+        for (int q = head + 2 * nv + tid; q < n; q += tile::NT) cval[base + q] = S.val[q];
+    }
+}
+
+// Prologue: the tile's rows and entries (contiguous in A and espan: one round
+// trip), the entry product prefix, the product -> entry map and the per-entry
+// row bucket ranges. Ends with the tables visible to the CTA.
+__device__ __forceinline__ TileDesc tile_prologue(TileSmem& S, int64_t k, const int64_t* __restrict__ arp,
+                                                  const double* __restrict__ aval,
+                                                  const uint64_t* __restrict__ espan,
+                                                  const int64_t* __restrict__ tr, const int64_t* __restrict__ te) {
+    constexpr int NT = tile::NT, EPT = tile::EPT;
+    const int tid = threadIdx.x;
+    TileDesc T;
+    T.k = k;
+    const int64_t trk = tr[k];
+    T.r0 = trk & ((int64_t(1) << 62) - 1);
+    T.big = (trk >> 62) != 0;
+    T.e0 = te[k];
+    T.R = static_cast<int>((tr[k + 1] & ((int64_t(1) << 62) - 1)) - T.r0);
+    T.E = static_cast<int>(te[k + 1] - T.e0);
+    T.ptile = 0;
+    if (T.big) return T;
+    for (int t = tid; t <= T.R; t += NT) S.re[t] = static_cast<int32_t>(arp[T.r0 + t] - T.e0);
+    const int per = (T.E + NT - 1) / NT;  // contiguous entries per thread (1 for typical tiles)
+    uint64_t sp[EPT];
+    double av[EPT];
+    int sum = 0;
+#pragma unroll
+    for (int c = 0; c < EPT; ++c) {
+        const int q = tid * per + c;
+        sp[c] = 0;
+        av[c] = 0.0;
+        if (c < per && q < T.E) {
+            sp[c] = espan[T.e0 + q];
+            av[c] = aval[T.e0 + q];
+        }
+        sum += static_cast<int>((sp[c] >> tile::SP_LEN) & 1023u);
+    }
+    int ptile;
+    int pre = tile_scan(sum, &ptile, S.ws[0]);
+    T.ptile = ptile;
+#pragma unroll
+    for (int c = 0; c < EPT; ++c) {
+        const int q = tid * per + c;
+        if (c < per && q < T.E) {
+            const int len = static_cast<int>((sp[c] >> tile::SP_LEN) & 1023u);
+            const int inrow = static_cast<int>((sp[c] >> tile::SP_IN) & 1023u);
+            const int prow = pre - inrow, pr = static_cast<int>(sp[c] >> tile::SP_PR);
+            S.ent[q] = TileEnt{static_cast<int64_t>(sp[c] & tile::SP_BS_MASK) - pre, av[c]};
+            S.ebin[q] = static_cast<uint32_t>(2 * prow) | (static_cast<uint32_t>(2 * pr) << 16);
+            S.epre[q] = pre;
+            for (int x = pre; x < pre + len; ++x) S.eof[x] = static_cast<uint16_t>(q);
+            pre += len;
+        }
+    }
+    if (tid == 0) {
+        S.epre[T.E] = ptile;
+        S.nlist = 0;
+    }
+    for (int q = tid; q <= ptile; q += NT) S.cnt[q] = 0u;  // ptile words = 2*ptile buckets
+    __syncthreads();
+    return T;
+}
+
+// Gathers of the tile's products x = tid + NT*j (all issued, none consumed).
+template <int NJ>
+__device__ __forceinline__ void tile_gather(const TileSmem& S, int ptile, const int32_t* __restrict__ bcol,
+                                            const double* __restrict__ bval, int32_t (&col)[NJ], double (&val)[NJ],
+                                            int (&aux)[NJ]) {
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        aux[j] = -1;
+        if (j * tile::NT >= ptile) break;  // uniform
+        const int x = threadIdx.x + tile::NT * j;
+        if (x < ptile) {
+            const int q = S.eof[x];
+            const int64_t u = S.ent[q].base + x;
+            aux[j] = q;
+            col[j] = __ldg(bcol + u);
+            val[j] = __ldg(bval + u);
+        }
+    }
+}
+
+// The tile's rows of C into the staging (sorted by (row, column), duplicates
+// combined in ascending k); S.rend[t] = end of row t. Returns the tile's nnz.
+template <int NJ>
+__device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int cshift, int32_t (&col)[NJ],
+                                            double (&val)[NJ], int (&aux)[NJ]) {
+    constexpr int NT = tile::NT;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ptile = T.ptile;
+    const int nj = (ptile + NT - 1) / NT;
+    // multiply (0 + av*bv, the reference's first accumulation) and count
+    int bk[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        bk[j] = -1;
+        if (j >= nj) break;
+        if (aux[j] >= 0) {
+            const int q = aux[j];
+            val[j] = dadd(0.0, dmul(S.ent[q].av, val[j]));
+            const uint32_t bi = S.ebin[q];
+            const int b = static_cast<int>(bi & 0xffffu) + bucket_of(col[j], cshift, static_cast<int>(bi >> 16));
+            bk[j] = b;
+            const int sh = (b & 1) << 4;
+            aux[j] = static_cast<int>((atomicAdd(&S.cnt[b >> 1], 1u << sh) >> sh) & 0xffffu);
+        }
+    }
+    __syncthreads();
+    // exclusive scan of the packed counters (odd-strided blocks: conflict-free)
+    {
+        const int W = ptile;
+        const int per = ((W + NT - 1) / NT) | 1;
+        const int w0 = tid * per;
+        uint32_t s = 0;
+        for (int q = 0; q < per; ++q)
+            if (w0 + q < W) s += S.cnt[w0 + q];
+        int tot;
+        const int cnt_s = static_cast<int>((s & 0xffffu) + (s >> 16));
+        uint32_t p2 = static_cast<uint32_t>(tile_scan(cnt_s, &tot, S.ws[1]));
+        for (int q = 0; q < per; ++q) {
+            if (w0 + q < W) {
+                const uint32_t wd = S.cnt[w0 + q];
+                S.cnt[w0 + q] = p2 * 0x10001u + (wd << 16);
+                p2 += (wd + (wd << 16)) >> 16;
+            }
+        }
+        if (tid == 0) S.cnt[W] = static_cast<uint32_t>(ptile);  // end of the last bucket
+    }
+    __syncthreads();
+    // place: alone in the bucket -> final; pairs ranked below; >= 3 -> list
+    unsigned pair = 0;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        if (j >= nj) break;
+        if (bk[j] >= 0) {
+            const int b = bk[j];
+            const uint32_t r = __funnelshift_r(S.cnt[b >> 1], S.cnt[(b >> 1) + 1], (b & 1) << 4);
+            const int st = static_cast<int>(r & 0xffffu), sz = static_cast<int>(r >> 16) - st;
+            const int slot = aux[j];
+            const int pos = st + slot;
+            S.col[pos] = col[j];
+            if (sz == 1) {
+                S.val[pos] = val[j];
+            } else {
+                S.xs[pos] = static_cast<uint16_t>(tid + NT * j);
+                if (sz == 2) {
+                    pair |= 1u << j;
+                    aux[j] = pos | (slot << 16);
+                } else {
+                    S.val[pos] = val[j];
+                    if (slot == 0) S.list[atomicAdd(&S.nlist, 1)] = r;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    // order shared buckets by (column, product id), detect duplicates. A pair
+    // reads only its partner's slot and, when swapped, writes only the
+    // partner's slot: no barrier is needed between the compare and the write.
+    bool dup = false;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        if (j >= nj) break;
+        if ((pair >> j) & 1u) {
+            const int pos = aux[j] & 0xffff, slot = aux[j] >> 16;
+            const int other = pos + 1 - 2 * slot;
+            const int32_t oc = S.col[other];
+            const int ox = S.xs[other];
+            const int x = tid + NT * j;
+            dup |= oc == col[j];
+            const int fpos = pos - slot + ((oc < col[j] || (oc == col[j] && ox < x)) ? 1 : 0);
+            if (fpos != pos) S.col[fpos] = col[j];
+            S.val[fpos] = val[j];
+        }
+    }
+    const int nlist = S.nlist;
+    for (int l = tid; l < nlist; l += NT) {
+        const int lo = static_cast<int>(S.list[l] & 0xffffu), hi = static_cast<int>(S.list[l] >> 16);
+        for (int a = lo + 1; a < hi; ++a) {
+            const int32_t ca = S.col[a];
+            const uint16_t xa = S.xs[a];
+            const double va = S.val[a];
+            int c = a - 1;
+            while (c >= lo && (S.col[c] > ca || (S.col[c] == ca && S.xs[c] > xa))) {
+                S.col[c + 1] = S.col[c];
+                S.xs[c + 1] = S.xs[c];
+                S.val[c + 1] = S.val[c];
+                --c;
+            }
+            S.col[c + 1] = ca;
+            S.xs[c + 1] = xa;
+            S.val[c + 1] = va;
+        }
+        for (int a = lo + 1; a < hi; ++a) dup |= S.col[a] == S.col[a - 1];
+    }
+    const int anydup = __syncthreads_or(dup);
+    if (!anydup) {
+        for (int t = tid; t < T.R; t += NT) S.rend[t] = S.epre[S.re[t + 1]];
+        return ptile;
+    }
+    // duplicates: combine runs of equal (row, column) in product-id order
+    // (= ascending k), compacting the staging in place
+    const int hw = (ptile >> 5) + 1;
+    for (int q = tid; q < hw + 1; q += NT) S.hbm[q] = 0u;
+    __syncthreads();
+    for (int t = tid; t < T.R; t += NT) {  // row starts are heads
+        const int ps = S.epre[S.re[t]];
+        if (S.epre[S.re[t + 1]] > ps) atomicOr(&S.hbm[ps >> 5], 1u << (ps & 31));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        const int x = tid + NT * j;  // a warp covers one bitmap word
+        bool head = false;
+        if (x < ptile) head = ((S.hbm[x >> 5] >> (x & 31)) & 1u) || x == 0 || S.col[x] != S.col[x - 1];
+        const unsigned hm = __ballot_sync(0xffffffffu, head);
+        __syncwarp();
+        if (lane == 0 && (warp * 32 + NT * j) < ptile) S.hbm[x >> 5] = hm;
+    }
+    __syncthreads();
+    int nnz;
+    {
+        const int v = tid < hw ? __popc(S.hbm[tid]) : 0;
+        const int hp = tile_scan(v, &nnz, S.ws[2]);
+        if (tid < hw) S.hpre[tid] = hp;
+        if (tid == 0) S.hpre[hw] = nnz;
+    }
+    __syncthreads();
+    int32_t oc[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        const int x = tid + NT * j;
+        aux[j] = -1;
+        oc[j] = 0;
+        if (x < ptile && ((S.hbm[x >> 5] >> (x & 31)) & 1u)) {
+            aux[j] = head_prefix(S, x);
+            oc[j] = S.col[x];
+            double s = S.val[x];
+            for (int u = x + 1; u < ptile && !((S.hbm[u >> 5] >> (u & 31)) & 1u); ++u) s = dadd(s, S.val[u]);
+            val[j] = s;
+        }
+    }
+    for (int t = tid; t < T.R; t += NT) S.rend[t] = head_prefix(S, S.epre[S.re[t + 1]]);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+        if (aux[j] >= 0) {
+            S.col[aux[j]] = oc[j];
+            S.val[aux[j]] = val[j];
+        }
+    return nnz;
+}
+
+// Exclusive prefix of tile k from the status words (all warps: 256
+// predecessors per round trip). Tile k only waits on tiles with smaller
+// tickets, whose CTAs publish their aggregates without waiting on anything,
+// so the chain always makes progress.
+__device__ __forceinline__ int64_t tile_look_back(TileSmem& S, uint64_t* status, int64_t k) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int64_t excl = 0;
+    for (int64_t j0 = k - 1; j0 >= 0; j0 -= tile::NT) {
+        const int64_t idx = j0 - tid;
+        uint64_t s = idx >= 0 ? ld_status(status + idx) : ST_INC;
+        unsigned inc, upto;
+        while (true) {
+            inc = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+            const unsigned none = __ballot_sync(0xffffffffu, (s >> 62) == 0);
+            upto = inc ? ((inc & (0u - inc)) << 1) - 1u : 0xffffffffu;  // lanes up to the first inclusive
+            if (!(none & upto)) break;
+            if ((s >> 62) == 0) s = ld_status(status + idx);
+        }
+        const int64_t v = warp_reduce_sum(((1u << lane) & upto) ? static_cast<int64_t>(s & ST_VAL) : int64_t(0));
+        if (lane == 0) {
+            S.lbs[warp] = v;
+            S.lbi[warp] = inc != 0;
+        }
+        __syncthreads();
+        bool found = false;
+#pragma unroll
+        for (int w = 0; w < tile::NW; ++w) {
+            if (!found) {
+                excl += S.lbs[w];
+                found = S.lbi[w] != 0;
+            }
+        }
+        __syncthreads();
+        if (found) break;
+    }
+    return excl;
+}
+
+#ifndef SPG_TILE_MINB
+#define SPG_TILE_MINB 2
+#endif
+// Persistent tile kernel. Per CTA, tiles come from a global ticket; for tile F
+// the order is: process F (its products already in registers) -> publish F's
+// aggregate -> prologue + gathers of the next tile -> look-back, row pointers
+// and copy-out of F (overlapping the next tile's gather latency).
+__global__ void __launch_bounds__(tile::NT, SPG_TILE_MINB) k_tile(
+    const int64_t* __restrict__ arp, const double* __restrict__ aval, const uint64_t* __restrict__ espan,
+    const int32_t* __restrict__ bcol, const double* __restrict__ bval, const int64_t* __restrict__ tr,
+    const int64_t* __restrict__ te, int64_t ntiles, unsigned long long* __restrict__ ticket, int cshift,
+    const int64_t* __restrict__ side_off, const int64_t* __restrict__ side_nnz,
+    const int32_t* __restrict__ side_col, const double* __restrict__ side_val, uint64_t* __restrict__ status,
+    int64_t* __restrict__ crp, int32_t* __restrict__ ccol, double* __restrict__ cval) {
+    constexpr int NT = tile::NT, NJ = tile::NJ;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TileSmem& S = *reinterpret_cast<TileSmem*>(smem_raw);
+    const int tid = threadIdx.x;
+
+    if (tid == 0) S.ticket = static_cast<int64_t>(atomicAdd(ticket, 1ull));
+    __syncthreads();
+    const int64_t k0 = S.ticket;
+    if (k0 >= ntiles) return;
+    int32_t col[NJ];
+    double val[NJ];
+    int aux[NJ];
+    TileDesc T = tile_prologue(S, k0, arp, aval, espan, tr, te);
+    if (!T.big) tile_gather<NJ>(S, T.ptile, bcol, bval, col, val, aux);
+    while (true) {
+        if (tid == 0) S.ticket = static_cast<int64_t>(atomicAdd(ticket, 1ull));
+        const int nnz = T.big ? 0 : tile_process<NJ>(S, T, cshift, col, val, aux);
+        const int64_t agg = T.big ? side_nnz[T.r0] : static_cast<int64_t>(nnz);
+        if (tid == 0) st_status(status + T.k, (T.k == 0 ? ST_INC : ST_AGG) | static_cast<uint64_t>(agg));
+        __syncthreads();  // staging + rend complete, ticket visible
+        const TileDesc F = T;  // tile to finish
+        const int64_t k2 = S.ticket;
+        const bool more = k2 < ntiles;
+        if (more) {
+            T = tile_prologue(S, k2, arp, aval, espan, tr, te);
+            if (!T.big) tile_gather<NJ>(S, T.ptile, bcol, bval, col, val, aux);
+        }
+        // finish F: offset, row pointers, copy-out
+        const int64_t base = tile_look_back(S, status, F.k);
+        if (tid == 0 && F.k > 0) st_status(status + F.k, ST_INC | static_cast<uint64_t>(base + agg));
+        if (F.big) {
+            const int64_t so = side_off[F.r0];
+            if (tid == 0) crp[F.r0 + 1] = base + agg;
+            for (int64_t q = tid; q < agg; q += NT) {
+                ccol[base + q] = side_col[so + q];
+                cval[base + q] = side_val[so + q];
+            }
+        } else {
+            for (int t = tid; t < F.R; t += NT) crp[F.r0 + t + 1] = base + S.rend[t];
+            tile_copy_out(S, nnz, base, ccol, cval, tid);
+        }
+        __syncthreads();
+        if (!more) break;
+    }
+}
+
 int grid_for(spg_ctx* ctx, int64_t n, int bs = 256) {
     const int64_t want = (n + bs - 1) / bs;
     const int64_t cap = int64_t(ctx->num_sms) * 16;
@@ -966,6 +1439,13 @@ int64_t spgemm_products(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
 
 namespace {
 constexpr int WPB = 8;  // warps per block of the warp kernels
+#ifndef SPG_NUM8_MINB
+#define SPG_NUM8_MINB 4
+#endif
+#ifndef SPG_NUM16_MINB
+#define SPG_NUM16_MINB 3
+#endif
+constexpr int NUM8_MINB = SPG_NUM8_MINB, NUM16_MINB = SPG_NUM16_MINB;
 
 int cshift_for(int64_t ncols) {
     int bits = 1;
@@ -974,12 +1454,11 @@ int cshift_for(int64_t ncols) {
 }
 }  // namespace
 
-spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
-    if (a->ncols != b->nrows)
-        fail(SPG_DIMENSION_ERROR,
-             "spgemm: a.ncols=" + std::to_string(a->ncols) + " != b.nrows=" + std::to_string(b->nrows));
+namespace {
+// Two-pass multiply (symbolic exact nnz, then numeric at exact offsets) with
+// warp-per-row kernels; kept as an alternative path (SPG_TWO_PASS=1).
+spg_csr* spgemm_two_pass(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     const int64_t m = a->nrows, n = b->ncols;
-    if (m == 0 || a->nnz == 0 || b->nnz == 0) return new_csr(ctx, m, n, 0);
     const int cshift = cshift_for(n);
 
     // 1: products per row + CTA/heavy row lists + total products
@@ -1008,12 +1487,6 @@ spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     SPG_CUDA(cudaMemcpyAsync(&products, total.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
     SPG_CUDA(cudaStreamSynchronize(ctx->stream));
     const int ncta = hc[2], nheavy = hc[3];
-
-    // single pass needs C sized by the products (an upper bound of nnz(C))
-    size_t free_b = 0, total_b = 0;
-    SPG_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const bool fused = ctx->force_two_pass == 0 &&
-                       static_cast<double>(products) * 12.0 < 0.6 * static_cast<double>(free_b);
 
     // heavy-row workspace plan (host side; heavy rows are few)
     std::vector<int64_t> hp_off(nheavy + 1, 0), he_off(nheavy + 1, 0), hb_off(nheavy + 1, 0);
@@ -1045,15 +1518,12 @@ spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     }
 
     const size_t cta_smem = sizeof(CtaSmem);
-    const size_t warp_smem = sizeof(WarpSlice) * WPB;
+    const size_t s8 = sizeof(WarpRowSmem<8>) * WPB, s16 = sizeof(WarpRowSmem<16>) * WPB;
     if (!ctx->tile_attr_set) {
         SPG_CUDA(cudaFuncSetAttribute(k_cta_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cta_smem));
         SPG_CUDA(cudaFuncSetAttribute(k_cta_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cta_smem));
-        SPG_CUDA(cudaFuncSetAttribute(k_warp_numeric<WPB, 8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(sizeof(WarpSliceT<8>) * WPB)));
-        SPG_CUDA(cudaFuncSetAttribute(k_warp_numeric<WPB, 16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(sizeof(WarpSliceT<16>) * WPB)));
-        SPG_CUDA(cudaFuncSetAttribute(k_warp_fused<WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)warp_smem));
+        SPG_CUDA(cudaFuncSetAttribute(k_warp_numeric<WPB, 8, NUM8_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s8));
+        SPG_CUDA(cudaFuncSetAttribute(k_warp_numeric<WPB, 16, NUM16_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s16));
         ctx->tile_attr_set = true;
     }
     const int gc = std::max(1, std::min(ncta, ctx->num_sms * 2));
@@ -1085,54 +1555,6 @@ spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
         SPG_LAUNCH_CHECK();
     };
 
-    if (fused) {
-        // side rows (CTA + heavy classes) first, into a products-bounded buffer
-        const int nside = ncta + nheavy;
-        DBuf<int64_t> side_off(ctx, m), sprod(ctx, nside + 1), soff(ctx, nside + 1);
-        SPG_CUDA(cudaMemsetAsync(side_off.get(), 0xff, m * sizeof(int64_t), ctx->stream));
-        int64_t side_total = 0;
-        if (nside) {
-            k_side_gather<<<grid_for(ctx, ncta), 256, 0, ctx->stream>>>(cta_list, cta_count, prod, sprod);
-            k_side_gather<<<grid_for(ctx, nheavy), 256, 0, ctx->stream>>>(heavy_list, heavy_count, prod,
-                                                                          sprod.get() + ncta);
-            SPG_LAUNCH_CHECK();
-            exclusive_scan_i64(ctx, sprod, soff, nside);
-            k_side_scatter<<<grid_for(ctx, ncta), 256, 0, ctx->stream>>>(cta_list, cta_count, soff, side_off);
-            k_side_scatter<<<grid_for(ctx, nheavy), 256, 0, ctx->stream>>>(heavy_list, heavy_count,
-                                                                           soff.get() + ncta, side_off);
-            SPG_LAUNCH_CHECK();
-            side_total = read_scalar(ctx, soff.get() + nside);
-        }
-        DBuf<int32_t> s_col(ctx, side_total);
-        DBuf<double> s_val(ctx, side_total);
-        if (nside) {
-            KTime kt(ctx, "spgemm_side_rows");
-            side_symbolic();
-            side_numeric(side_off, s_col, s_val);
-        }
-        spg_csr* c = new_csr(ctx, m, n, -1);
-        c->colind = dalloc<int32_t>(ctx, products);
-        c->values = dalloc<double>(ctx, products);
-        DBuf<uint64_t> status(ctx, m);
-        DBuf<unsigned long long> ticket(ctx, 1);
-        SPG_CUDA(cudaMemsetAsync(status.get(), 0, m * sizeof(uint64_t), ctx->stream));
-        SPG_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned long long), ctx->stream));
-        SPG_CUDA(cudaMemsetAsync(c->rowptr, 0, sizeof(int64_t), ctx->stream));
-        int occ = 1;
-        SPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_warp_fused<WPB>, WPB * 32, warp_smem));
-        const int64_t wblocks = (m + WPB - 1) / WPB;
-        const int gf = static_cast<int>(std::min<int64_t>(wblocks, int64_t(ctx->num_sms) * std::max(occ, 1)));
-        {
-            KTime kt(ctx, "spgemm_numeric");
-            k_warp_fused<WPB><<<gf, WPB * 32, warp_smem, ctx->stream>>>(
-                a->rowptr, a->colind, a->values, b->rowptr, b->colind, b->values, m, cshift, side_off, rnnz, s_col,
-                s_val, ticket, status, c->rowptr, c->colind, c->values);
-            SPG_LAUNCH_CHECK();
-        }
-        c->nnz = read_scalar(ctx, c->rowptr + m);
-        return c;
-    }
-
     // two-pass: symbolic (exact nnz) then numeric at exact offsets
     const int64_t wblocks = (m + WPB - 1) / WPB;
     auto grid_of = [&](const void* fn, size_t smem) {
@@ -1162,15 +1584,14 @@ spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     c->values = dalloc<double>(ctx, c->nnz);
     {
         KTime kt(ctx, "spgemm_numeric");
-        const size_t s8 = sizeof(WarpSliceT<8>) * WPB, s16 = sizeof(WarpSliceT<16>) * WPB;
         {
         KTime k8(ctx, "num_w8");
-        k_warp_numeric<WPB, 8, 3><<<grid_of((const void*)k_warp_numeric<WPB, 8, 3>, s8), WPB * 32, s8,
+        k_warp_numeric<WPB, 8, NUM8_MINB><<<grid_of((const void*)k_warp_numeric<WPB, 8, NUM8_MINB>, s8), WPB * 32, s8,
                                     ctx->stream>>>(a->rowptr, a->colind, a->values, b->rowptr, b->colind, b->values,
                                                    list8, counts.get(), cshift, c->rowptr, c->colind, c->values);
         }
         KTime k16(ctx, "num_w16");
-        k_warp_numeric<WPB, 16, 2><<<grid_of((const void*)k_warp_numeric<WPB, 16, 2>, s16), WPB * 32, s16,
+        k_warp_numeric<WPB, 16, NUM16_MINB><<<grid_of((const void*)k_warp_numeric<WPB, 16, NUM16_MINB>, s16), WPB * 32, s16,
                                      ctx->stream>>>(a->rowptr, a->colind, a->values, b->rowptr, b->colind, b->values,
                                                     list16, counts.get() + 1, cshift, c->rowptr, c->colind,
                                                     c->values);
@@ -1178,6 +1599,177 @@ spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
         side_numeric(c->rowptr, c->colind, c->values);
     }
     return c;
+}
+
+// Single-pass tiled multiply (the default).
+spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
+    const int64_t m = a->nrows, n = b->ncols;
+    const int cshift = cshift_for(n);
+    // 1: products, entry spans, row weights, BIG-row lists
+    DBuf<int64_t> prod(ctx, m), wt(ctx, m), total(ctx, 1);
+    DBuf<uint64_t> espan(ctx, a->nnz);
+    DBuf<int32_t> lists(ctx, 2 * m), counts(ctx, 2);
+    int32_t* cta_list = lists.get();
+    int32_t* heavy_list = lists.get() + m;
+    SPG_CUDA(cudaMemsetAsync(counts.get(), 0, 2 * sizeof(int32_t), ctx->stream));
+    {
+        KTime kt(ctx, "row_prep");
+        k_row_prep<<<grid_for(ctx, 32 * m), 256, 0, ctx->stream>>>(a->rowptr, a->colind, b->rowptr, m, prod, wt,
+                                                                   espan, lists, counts);
+        SPG_LAUNCH_CHECK();
+    }
+    {
+        size_t tmp = 0;
+        SPG_CUDA(cub::DeviceReduce::Sum(nullptr, tmp, prod.get(), total.get(), m, ctx->stream));
+        DBuf<unsigned char> t(ctx, tmp);
+        SPG_CUDA(cub::DeviceReduce::Sum(t.get(), tmp, prod.get(), total.get(), m, ctx->stream));
+    }
+    // 2: tile starts (weight windows; BIG rows alone)
+    DBuf<int64_t> wpre(ctx, m + 1), flag(ctx, m), fpos(ctx, m + 1);
+    exclusive_scan_i64(ctx, wt, wpre, m);
+    int32_t hc[2];
+    int64_t products = 0;
+    SPG_CUDA(cudaMemcpyAsync(hc, counts.get(), sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
+    SPG_CUDA(cudaMemcpyAsync(&products, total.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    {
+        KTime kt(ctx, "tile_setup");
+        k_tile_flags<<<grid_for(ctx, m), 256, 0, ctx->stream>>>(wpre, prod, a->rowptr, m, flag);
+        SPG_LAUNCH_CHECK();
+    }
+    SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+    const int ncta = hc[0], nheavy = hc[1], nside = ncta + nheavy;
+
+    // 3: BIG rows into a side buffer (symbolic, offsets, numeric)
+    DBuf<int64_t> rnnz(ctx, m), side_off(ctx, m);
+    std::vector<int64_t> hp_off(nheavy + 1, 0), he_off(nheavy + 1, 0), hb_off(nheavy + 1, 0);
+    if (nheavy) {
+        DBuf<int64_t> info(ctx, 2 * int64_t(nheavy));
+        k_heavy_info<<<grid_for(ctx, nheavy), 256, 0, ctx->stream>>>(heavy_list, nheavy, prod, a->rowptr, info);
+        SPG_LAUNCH_CHECK();
+        std::vector<int64_t> hinfo(2 * size_t(nheavy));
+        SPG_CUDA(cudaMemcpyAsync(hinfo.data(), info.get(), hinfo.size() * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+        SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (int h = 0; h < nheavy; ++h) {
+            hp_off[h + 1] = hp_off[h] + hinfo[2 * h];
+            he_off[h + 1] = he_off[h] + hinfo[2 * h + 1] + 1;
+            hb_off[h + 1] = hb_off[h] + (hinfo[2 * h] + BUCKET_LOAD - 1) / BUCKET_LOAD + 1;
+        }
+    }
+    DBuf<int64_t> d_hp(ctx, nheavy + 1), d_he(ctx, nheavy + 1), d_hb(ctx, nheavy + 1);
+    DBuf<int64_t> w_epre(ctx, he_off[nheavy]);
+    DBuf<int32_t> w_col(ctx, hp_off[nheavy]), w_bkt(ctx, hp_off[nheavy]), w_perm(ctx, hp_off[nheavy]);
+    DBuf<double> w_val(ctx, hp_off[nheavy]);
+    DBuf<int64_t> w_boff(ctx, hb_off[nheavy]), w_bcnt(ctx, hb_off[nheavy]);
+    HeavyWs hws{};
+    if (nheavy) {
+        SPG_CUDA(cudaMemcpyAsync(d_hp.get(), hp_off.data(), (nheavy + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+        SPG_CUDA(cudaMemcpyAsync(d_he.get(), he_off.data(), (nheavy + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+        SPG_CUDA(cudaMemcpyAsync(d_hb.get(), hb_off.data(), (nheavy + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+        hws = HeavyWs{w_epre, w_col, w_val, w_bkt, w_perm, w_boff, w_bcnt};
+    }
+    const size_t cta_smem = sizeof(CtaSmem);
+    if (!ctx->tile_attr_set) {
+        SPG_CUDA(cudaFuncSetAttribute(k_cta_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cta_smem));
+        SPG_CUDA(cudaFuncSetAttribute(k_cta_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cta_smem));
+        SPG_CUDA(cudaFuncSetAttribute(k_warp_numeric<WPB, 8, NUM8_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sizeof(WarpRowSmem<8>) * WPB)));
+        SPG_CUDA(cudaFuncSetAttribute(k_warp_numeric<WPB, 16, NUM16_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sizeof(WarpRowSmem<16>) * WPB)));
+        SPG_CUDA(cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem)));
+        ctx->tile_attr_set = true;
+    }
+    int64_t side_total = 0;
+    DBuf<int64_t> sn(ctx, nside + 1), so(ctx, nside + 1);
+    if (nside) {
+        KTime kt(ctx, "side_rows");
+        const int gc = std::max(1, std::min(ncta, ctx->num_sms * 2));
+        if (ncta)
+            k_cta_rows<false><<<gc, NT, cta_smem, ctx->stream>>>(a->rowptr, a->colind, a->values, b->rowptr,
+                                                                 b->colind, b->values, prod, cta_list, counts.get(),
+                                                                 rnnz, nullptr, nullptr, nullptr);
+        if (nheavy)
+            k_heavy<false><<<nheavy, NT, 0, ctx->stream>>>(a->rowptr, a->colind, a->values, b->rowptr, b->colind,
+                                                           b->values, heavy_list, d_hp, d_he, d_hb, hws, rnnz, nullptr,
+                                                           nullptr, nullptr);
+        SPG_LAUNCH_CHECK();
+        if (ncta) k_side_gather<<<grid_for(ctx, ncta), 256, 0, ctx->stream>>>(cta_list, ncta, rnnz, sn);
+        if (nheavy) k_side_gather<<<grid_for(ctx, nheavy), 256, 0, ctx->stream>>>(heavy_list, nheavy, rnnz, sn.get() + ncta);
+        SPG_LAUNCH_CHECK();
+        exclusive_scan_i64(ctx, sn, so, nside);
+        if (ncta) k_side_scatter<<<grid_for(ctx, ncta), 256, 0, ctx->stream>>>(cta_list, ncta, so, side_off);
+        if (nheavy)
+            k_side_scatter<<<grid_for(ctx, nheavy), 256, 0, ctx->stream>>>(heavy_list, nheavy, so.get() + ncta, side_off);
+        SPG_LAUNCH_CHECK();
+        side_total = read_scalar(ctx, so.get() + nside);
+    }
+    DBuf<int32_t> s_col(ctx, side_total);
+    DBuf<double> s_val(ctx, side_total);
+    if (nside) {
+        KTime kt(ctx, "side_rows");
+        const int gc = std::max(1, std::min(ncta, ctx->num_sms * 2));
+        if (ncta)
+            k_cta_rows<true><<<gc, NT, cta_smem, ctx->stream>>>(a->rowptr, a->colind, a->values, b->rowptr, b->colind,
+                                                                b->values, prod, cta_list, counts.get(), nullptr,
+                                                                side_off, s_col, s_val);
+        if (nheavy)
+            k_heavy<true><<<nheavy, NT, 0, ctx->stream>>>(a->rowptr, a->colind, a->values, b->rowptr, b->colind,
+                                                          b->values, heavy_list, d_hp, d_he, d_hb, hws, nullptr,
+                                                          side_off, s_col, s_val);
+        SPG_LAUNCH_CHECK();
+    }
+    // 4: tiles
+    exclusive_scan_i64(ctx, flag, fpos, m);
+    const int64_t ntiles = read_scalar(ctx, fpos.get() + m);
+    DBuf<int64_t> tr(ctx, ntiles + 1), te(ctx, ntiles + 1);
+    DBuf<uint64_t> status(ctx, ntiles);
+    {
+        KTime kt(ctx, "tile_setup");
+        k_tile_scatter<<<grid_for(ctx, m + 1), 256, 0, ctx->stream>>>(flag, fpos,
+                                                                      prod, a->rowptr, m, tr, te);
+        SPG_LAUNCH_CHECK();
+    }
+    SPG_CUDA(cudaMemsetAsync(status.get(), 0, ntiles * sizeof(uint64_t), ctx->stream));
+    DBuf<unsigned long long> ticket(ctx, 1);
+    SPG_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned long long), ctx->stream));
+    spg_csr* c = new_csr(ctx, m, n, -1);
+    c->colind = dalloc<int32_t>(ctx, products);  // upper bound of nnz(C)
+    c->values = dalloc<double>(ctx, products);
+    SPG_CUDA(cudaMemsetAsync(c->rowptr, 0, sizeof(int64_t), ctx->stream));
+    int occ = 1;
+    SPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile, tile::NT, sizeof(TileSmem)));
+    const int grid = static_cast<int>(std::min<int64_t>(ntiles, int64_t(ctx->num_sms) * std::max(occ, 1)));
+    {
+        KTime kt(ctx, "spgemm_tile");
+        k_tile<<<grid, tile::NT, sizeof(TileSmem), ctx->stream>>>(a->rowptr, a->values, espan, b->colind, b->values,
+                                                                  tr, te, ntiles, ticket, cshift, side_off, rnnz, s_col,
+                                                                  s_val, status, c->rowptr, c->colind, c->values);
+        SPG_LAUNCH_CHECK();
+    }
+    c->nnz = read_scalar(ctx, c->rowptr + m);
+    return c;
+}
+}  // namespace
+
+#ifdef SPG_TILE_PROF
+extern "C" int spg_dev_tile_prof(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, g_tile_prof, 16 * sizeof(unsigned long long));
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_tile_prof, z, sizeof(z));
+    return 0;
+}
+#endif
+
+spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
+    if (a->ncols != b->nrows)
+        fail(SPG_DIMENSION_ERROR,
+             "spgemm: a.ncols=" + std::to_string(a->ncols) + " != b.nrows=" + std::to_string(b->nrows));
+    const int64_t m = a->nrows, n = b->ncols;
+    if (m == 0 || a->nnz == 0 || b->nnz == 0) return new_csr(ctx, m, n, 0);
+    if (n > (int64_t(1) << 31)) fail(SPG_PARAMETER_ERROR, "spgemm: b.ncols must be < 2^31 (int32 column indices)");
+    // the tile path packs B row starts in 34 bits (always true on one GPU)
+    if (ctx->two_pass || b->nnz >= (int64_t(1) << tile::SP_BS)) return spgemm_two_pass(ctx, a, b);
+    return spgemm_tiled(ctx, a, b);
 }
 
 }  // namespace spgb

@@ -31,13 +31,13 @@ def gpu_mul(dev, a, b, check=True):
 
 @pytest.fixture(scope="module")
 def dev2():
-    """A second context on the single-pass (decoupled look-back) path."""
+    """A second context on the two-pass (symbolic + numeric) warp kernels."""
     import os
-    os.environ["SPG_FUSED"] = "1"
+    os.environ["SPG_TWO_PASS"] = "1"
     try:
         d = spg.Device(0)
     finally:
-        del os.environ["SPG_FUSED"]
+        del os.environ["SPG_TWO_PASS"]
     yield d
     d.close()
 
@@ -110,6 +110,66 @@ def test_heavy_and_skewed_rows(dev, dev2):
     ref = O.port_spgemm(r, r)
     assert same(gpu_mul(dev, r, r), ref)
     assert same(gpu_mul(dev2, r, r), ref)
+
+
+def _rows_with(products_per_row, entries, ncols_b, seed, b_len=None):
+    """A (one row per target) x B with B rows of b_len entries over ncols_b
+    columns: row r gets entries[r] A entries whose B rows sum to products_per_row[r]."""
+    rng = np.random.default_rng(seed)
+    nb_rows = 4096
+    b_rp = [0]
+    b_ci, b_va = [], []
+    lens = rng.integers(1, 40, nb_rows) if b_len is None else np.full(nb_rows, b_len)
+    for k in range(nb_rows):
+        L = int(min(lens[k], ncols_b))
+        cols = np.sort(rng.choice(ncols_b, L, replace=False))
+        b_ci += list(cols); b_va += list(rng.random(L) + 0.25); b_rp.append(len(b_ci))
+    b_rp = np.array(b_rp, np.int64)
+    blen = np.diff(b_rp)
+    a_rp, a_ci = [0], []
+    for p, e in zip(products_per_row, entries):
+        # greedy: pick e distinct B rows whose lengths sum to p (last one adjusted via a row of the exact length)
+        ks = []
+        left = p
+        cand = rng.permutation(nb_rows)
+        for k in cand:
+            if len(ks) == e - 1:
+                break
+            if blen[k] <= left - (e - 1 - len(ks)):
+                ks.append(int(k)); left -= int(blen[k])
+        exact = [int(k) for k in np.nonzero(blen == left)[0] if int(k) not in ks]
+        if left > 0 and exact:
+            ks.append(exact[0])
+        a_ci += sorted(ks); a_rp.append(len(a_ci))
+    a_rp = np.array(a_rp, np.int64)
+    a = O.Csr(len(products_per_row), nb_rows, a_rp, np.array(a_ci, np.int64), rng.random(len(a_ci)) + 0.5)
+    b = O.Csr(nb_rows, ncols_b, b_rp, np.array(b_ci, np.int64), np.array(b_va))
+    return a, b
+
+
+@pytest.mark.parametrize("ncols_b", [64, 700, 1 << 20])
+def test_row_class_boundaries_and_duplicates(dev, dev2, ncols_b):
+    # products per row around the class edges (256/257, 512/513, 4096/4097) with
+    # 1..33 entries; small ncols_b makes nearly every product a duplicate
+    targets = [1, 2, 31, 32, 33, 255, 256, 257, 300, 511, 512, 513, 1000, 4095, 4096, 4097, 6000]
+    ents = [1, 2, 5, 16, 32, 33, 8, 31, 32, 20, 32, 33, 40, 32, 200, 300, 500]
+    rows, es = [], []
+    for t in targets:
+        for e in ents:
+            if e <= t:
+                rows.append(t); es.append(e)
+    a, b = _rows_with(rows, es, ncols_b, seed=ncols_b)
+    ref = O.port_spgemm(a, b)
+    assert same(gpu_mul(dev, a, b), ref)
+    assert same(gpu_mul(dev2, a, b), ref)
+
+
+def test_all_one_column(dev):
+    # every product of every row lands in the same column (one bucket)
+    n = 600
+    a = O.port_gen_erdos_renyi(n, 0.05, 3)
+    b = O.Csr(n, 3, np.arange(n + 1, dtype=np.int64), np.full(n, 1, np.int64), np.linspace(-1, 1, n))
+    assert same(gpu_mul(dev, a, b), O.port_spgemm(a, b))
 
 
 def test_rectangular_and_transpose(dev):
