@@ -821,7 +821,10 @@ __global__ void k_heavy_info(const int32_t* __restrict__ rows, int n, const int6
 // (BIG rows) are multiplied beforehand into a side buffer by the CTA / heavy
 // row kernels and occupy a tile of their own that only copies.
 namespace tile {
-constexpr int NT = 256;                         // threads per CTA
+#ifndef SPG_TILE_NT
+#define SPG_TILE_NT 256
+#endif
+constexpr int NT = SPG_TILE_NT;                 // threads per CTA
 constexpr int NW = NT / 32;
 constexpr int SMALL_P = 512;                    // a tile row has <= SMALL_P products
 constexpr int SMALL_E = 64;                     // ... and <= SMALL_E entries
@@ -1055,6 +1058,30 @@ __device__ __forceinline__ void tile_copy_out(const TileSmem& S, int n, int64_t 
     }
 }
 
+#ifdef SPG_TILE_PROF
+// Dev instrumentation (-DSPG_TILE_PROF): per-phase clock64 totals of thread 0.
+__device__ unsigned long long g_tile_prof[16];
+__shared__ unsigned long long s_tp_last, s_tp_acc[16];
+#define TPROF_DECL                                            \
+    if (threadIdx.x == 0) {                                   \
+        s_tp_last = clock64();                                \
+        for (int i_ = 0; i_ < 16; ++i_) s_tp_acc[i_] = 0;     \
+    }
+#define TPROF(i)                                              \
+    if (threadIdx.x == 0) {                                   \
+        const unsigned long long t_ = clock64();              \
+        s_tp_acc[i] += t_ - s_tp_last;                        \
+        s_tp_last = t_;                                       \
+    }
+#define TPROF_FLUSH                                                              \
+    if (threadIdx.x == 0)                                                        \
+        for (int i_ = 0; i_ < 16; ++i_) atomicAdd(&g_tile_prof[i_], s_tp_acc[i_]);
+#else
+#define TPROF_DECL
+#define TPROF(i)
+#define TPROF_FLUSH
+#endif
+
 // Prologue: the tile's rows and entries (contiguous in A and espan: one round
 // trip), the entry product prefix, the product -> entry map and the per-entry
 // row bucket ranges. Ends with the tables visible to the CTA.
@@ -1090,6 +1117,7 @@ __device__ __forceinline__ TileDesc tile_prologue(TileSmem& S, int64_t k, const 
         }
         sum += static_cast<int>((sp[c] >> tile::SP_LEN) & 1023u);
     }
+    TPROF(15)
     int ptile;
     int pre = tile_scan(sum, &ptile, S.ws[0]);
     T.ptile = ptile;
@@ -1161,7 +1189,9 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
             aux[j] = static_cast<int>((atomicAdd(&S.cnt[b >> 1], 1u << sh) >> sh) & 0xffffu);
         }
     }
+    TPROF(8)
     __syncthreads();
+    TPROF(9)
     // exclusive scan of the packed counters (odd-strided blocks: conflict-free)
     {
         const int W = ptile;
@@ -1183,6 +1213,7 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
         if (tid == 0) S.cnt[W] = static_cast<uint32_t>(ptile);  // end of the last bucket
     }
     __syncthreads();
+    TPROF(10)
     // place: alone in the bucket -> final; pairs ranked below; >= 3 -> list
     unsigned pair = 0;
 #pragma unroll
@@ -1209,7 +1240,9 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
             }
         }
     }
+    TPROF(11)
     __syncthreads();
+    TPROF(12)
     // order shared buckets by (column, product id), detect duplicates. A pair
     // reads only its partner's slot and, when swapped, writes only the
     // partner's slot: no barrier is needed between the compare and the write.
@@ -1249,7 +1282,9 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
         }
         for (int a = lo + 1; a < hi; ++a) dup |= S.col[a] == S.col[a - 1];
     }
+    TPROF(13)
     const int anydup = __syncthreads_or(dup);
+    TPROF(14)
     if (!anydup) {
         for (int t = tid; t < T.R; t += NT) S.rend[t] = S.epre[S.re[t + 1]];
         return ptile;
@@ -1363,6 +1398,7 @@ __global__ void __launch_bounds__(tile::NT, SPG_TILE_MINB) k_tile(
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TileSmem& S = *reinterpret_cast<TileSmem*>(smem_raw);
     const int tid = threadIdx.x;
+    TPROF_DECL
 
     if (tid == 0) S.ticket = static_cast<int64_t>(atomicAdd(ticket, 1ull));
     __syncthreads();
@@ -1375,19 +1411,25 @@ __global__ void __launch_bounds__(tile::NT, SPG_TILE_MINB) k_tile(
     if (!T.big) tile_gather<NJ>(S, T.ptile, bcol, bval, col, val, aux);
     while (true) {
         if (tid == 0) S.ticket = static_cast<int64_t>(atomicAdd(ticket, 1ull));
+        TPROF(0)
         const int nnz = T.big ? 0 : tile_process<NJ>(S, T, cshift, col, val, aux);
+        TPROF(1)
         const int64_t agg = T.big ? side_nnz[T.r0] : static_cast<int64_t>(nnz);
         if (tid == 0) st_status(status + T.k, (T.k == 0 ? ST_INC : ST_AGG) | static_cast<uint64_t>(agg));
         __syncthreads();  // staging + rend complete, ticket visible
+        TPROF(2)
         const TileDesc F = T;  // tile to finish
         const int64_t k2 = S.ticket;
         const bool more = k2 < ntiles;
         if (more) {
             T = tile_prologue(S, k2, arp, aval, espan, tr, te);
+            TPROF(3)
             if (!T.big) tile_gather<NJ>(S, T.ptile, bcol, bval, col, val, aux);
+            TPROF(4)
         }
         // finish F: offset, row pointers, copy-out
         const int64_t base = tile_look_back(S, status, F.k);
+        TPROF(5)
         if (tid == 0 && F.k > 0) st_status(status + F.k, ST_INC | static_cast<uint64_t>(base + agg));
         if (F.big) {
             const int64_t so = side_off[F.r0];
@@ -1400,9 +1442,12 @@ __global__ void __launch_bounds__(tile::NT, SPG_TILE_MINB) k_tile(
             for (int t = tid; t < F.R; t += NT) crp[F.r0 + t + 1] = base + S.rend[t];
             tile_copy_out(S, nnz, base, ccol, cval, tid);
         }
+        TPROF(6)
         __syncthreads();
+        TPROF(7)
         if (!more) break;
     }
+    TPROF_FLUSH
 }
 
 int grid_for(spg_ctx* ctx, int64_t n, int bs = 256) {

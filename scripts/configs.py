@@ -1,0 +1,190 @@
+"""Measured runs of every BASELINE.json config on one B200.
+
+    python scripts/configs.py [--configs 1,2,3,4,5] [--rmat-scale 22] [--reps 3]
+
+One JSON line per config: products, nnz(C), ms per C = A*B (CUDA events around
+the C-ABI multiply, inputs resident in HBM, best and median of --reps after a
+warm-up), GFLOP/s = 2*products/t, and a parity verdict:
+  config 1     full C vs the CPU oracle (bit-exact)
+  config 2/4/5 nnz + sampled rows vs the reference digests (tests/golden)
+  config 3     R-MAT Graph500 (a,b,c,d) = (.57,.19,.19,.05), edge factor 16,
+               symmetric random permutation; C does not fit one GPU at scale 22
+               (~7e10 nnz), so C is produced in row batches bounded by products
+               and discarded; sampled rows are checked against the oracle
+               multiplying the same rows of A by A (rows of C depend only on
+               rows of A, so the check is exact).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2603_21444_b200 as spg  # noqa: E402
+
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+
+def golden(k):
+    with open(os.path.join(GOLD, f"config{k}.json")) as f:
+        return json.load(f)
+
+
+def row_products(a, b):
+    blen = np.diff(np.asarray(b.rowptr, np.int64))
+    per_entry = blen[np.asarray(a.colind, np.int64)]
+    rp = np.asarray(a.rowptr, np.int64)
+    out = np.zeros(int(a.nrows), np.int64)
+    nz = np.diff(rp) > 0
+    if per_entry.size:
+        out[nz] = np.add.reduceat(per_entry, rp[:-1][nz])
+    return out
+
+
+def timed(dev, fn, reps):
+    import ctypes as C
+    from paper_2603_21444_b200 import _capi
+    L = _capi.lib()
+    fn()  # warm-up
+    dev.synchronize()
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        r = fn()
+        dev.synchronize()
+        ts.append((time.perf_counter() - t0) * 1e3)
+        del r
+    return min(ts), statistics.median(ts)
+
+
+def samples_ok(c, g, exact=True, tol=1e-12):
+    bad = 0
+    for i, row in g["sample_rows"].items():
+        i = int(i)
+        lo, hi = int(c.rowptr[i]), int(c.rowptr[i + 1])
+        got, ref = np.asarray(c.values[lo:hi]), np.asarray(row["vals"])
+        if c.colind[lo:hi].tolist() != row["cols"]:
+            bad += 1
+        elif exact and not np.array_equal(got, ref):
+            bad += 1
+        elif not np.all(np.abs(got - ref) <= tol * np.maximum(np.abs(got), np.abs(ref))):
+            bad += 1
+    return bad == 0
+
+
+def run_simple(dev, k, a, b, reps, desc):
+    da = dev.upload(a)
+    db = da if b is a else dev.upload(b)
+    products = dev.products(da, db)
+    holder = {}
+
+    def go():
+        holder["c"] = dev.spgemm(da, db)
+        return holder["c"]
+
+    best, med = timed(dev, go, reps)
+    c = holder["c"]
+    line = {"config": k, "workload": desc, "products": products, "nnz_C": c.nnz, "ms_best": round(best, 3),
+            "ms_median": round(med, 3), "gflops": round(2 * products / best / 1e6, 2)}
+    return line, da, db, c
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="1,2,3,4,5")
+    ap.add_argument("--rmat-scale", type=int, default=22)
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--batch-products", type=float, default=2.5e9)
+    args = ap.parse_args()
+    dev = spg.Device(0)
+    want = [int(x) for x in args.configs.split(",")]
+    for k in want:
+        t0 = time.time()
+        if k == 1:
+            import oracle as O
+            a = spg.gen_erdos_renyi(16384, 8.0 / 16384, 1)
+            line, da, db, c = run_simple(dev, 1, a, a, args.reps, "ER n=16384, 8/row, C=A*A")
+            ref = O.ref_spgemm_local(a, a) if O.ref_available() else O.port_spgemm(a, a)
+            h = c.download()
+            line["parity"] = bool(np.array_equal(h.rowptr, ref.rowptr) and np.array_equal(h.colind, ref.colind)
+                                  and np.array_equal(h.values, ref.values))
+        elif k in (2, 4, 5):
+            g = golden(k)
+            if k == 2:
+                a = spg.gen_erdos_renyi(1 << 22, 16.0 / (1 << 22), 1)
+                b, desc = a, "ER n=2^22, 16/row, C=A*A"
+            elif k == 4:
+                m = spg.gen_erdos_renyi(1 << 21, 16.0 / (1 << 21), 1)
+                dm = dev.upload(m)
+                dev.column_normalize(dm)
+                a = dm.download()
+                b, desc = a, "MCL: M=column_normalize(ER 2^21, 16/row); C=M*M"
+            else:
+                a = spg.gen_erdos_renyi_rect(1 << 22, 1 << 18, 2.0 ** -16, 5)
+                b, desc = spg.transpose(a), "k-mer A*A^T, A = ER 2^22 x 2^18, 4/row"
+            line, da, db, c = run_simple(dev, k, a, b, args.reps, desc)
+            h = c.download()
+            line["parity"] = bool(int(h.nnz) == g["nnz"] and samples_ok(h, g))
+            if k == 4:
+                # MCL post-step: column_normalize + prune(0.002), timed separately
+                t1 = time.perf_counter()
+                dev.column_normalize(c)
+                p = dev.prune(c, 0.002)
+                dev.synchronize()
+                line["post_ms"] = round((time.perf_counter() - t1) * 1e3, 3)
+                line["pruned_nnz"] = p.nnz
+                line["parity"] = line["parity"] and p.nnz == g["pruned"]["nnz"]
+        elif k == 3:
+            import oracle as O
+            s = args.rmat_scale
+            a = spg.gen_rmat(s, 16, 1, 2)
+            rp = row_products(a, a)
+            total = int(rp.sum())
+            da = dev.upload(a)
+            # row batches bounded by products (C of a batch stays on the device)
+            cum = np.cumsum(rp)
+            cuts = [0]
+            while cuts[-1] < a.nrows:
+                base = cum[cuts[-1] - 1] if cuts[-1] > 0 else 0
+                nxt = int(np.searchsorted(cum, base + args.batch_products, side="right"))
+                cuts.append(max(nxt, cuts[-1] + 1) if nxt < a.nrows else int(a.nrows))
+            dev.synchronize()
+            nnz = 0
+            t1 = time.perf_counter()
+            for r0, r1 in zip(cuts[:-1], cuts[1:]):
+                ab = dev.extract(da, r0, r1, 0, int(a.ncols))
+                cb = dev.spgemm(ab, da)
+                nnz += cb.nnz
+                del ab, cb
+            dev.synchronize()
+            ms = (time.perf_counter() - t1) * 1e3
+            # parity: sampled rows (heaviest row + random rows) vs the oracle
+            rng = np.random.default_rng(7)
+            rows = sorted(set([int(np.argmax(rp))] + rng.choice(a.nrows, 24, replace=False).tolist()))
+            ok = True
+            for i in rows:
+                if rp[i] > 5e7:
+                    continue
+                ai = spg.extract(a, (i, i + 1, 0, int(a.ncols)))
+                ref = O.port_spgemm(ai, a)
+                got = dev.spgemm(dev.upload(ai), da).download()
+                ok &= bool(np.array_equal(got.colind, ref.colind) and np.array_equal(got.values, ref.values))
+            line = {"config": 3, "workload": f"R-MAT scale {s}, edge factor 16, C=A*A (row-batched)",
+                    "nnz_A": int(a.nnz), "products": total, "nnz_C": int(nnz), "batches": len(cuts) - 1,
+                    "max_row_products": int(rp.max()), "ms_best": round(ms, 3), "ms_median": round(ms, 3),
+                    "gflops": round(2 * total / ms / 1e6, 2), "parity": ok, "parity_rows": len(rows)}
+        else:
+            continue
+        line["wall_s"] = round(time.time() - t0, 1)
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()
