@@ -399,6 +399,10 @@ def ours_multi(args):
     ledger = sd.ledger_for(a, a, grid)
     recv_bytes = int(ledger[:, 1, :, 2].sum(axis=1).max())
     tl_mean = np.mean(np.stack(tls), axis=0)  # [q, 4] ms
+    if os.environ.get("SPG_BENCH_DEBUG"):
+        print(f"[rank {rank}] ms/step {ms_local:.3f} timeline(q x [exchange, exposed wait, multiply, merge]) "
+              f"{np.round(tl_mean, 3).tolist()} kernels {{{', '.join(f'{k}: {v[1] / max(1, v[0]):.3f}' for k, v in kt.items())}}}",
+              file=sys.stderr, flush=True)
     exch_ms = float(tl_mean[:, 0].sum())
     if rank == 0:
         peak, peak_kind = measured_peaks()

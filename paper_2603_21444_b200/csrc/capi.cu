@@ -129,6 +129,7 @@ spg_status spg_finalize(spg_ctx* ctx) {
     return guard([&] {
         if (!ctx) return;
         DeviceScope ds(ctx->device);
+        big_cache_release(ctx);
         cudaStreamSynchronize(ctx->stream);
         for (auto& r : ctx->timer.pending) {
             cudaEventDestroy(r.start);

@@ -289,13 +289,71 @@ spg_csr* new_csr(spg_ctx* ctx, int64_t nrows, int64_t ncols, int64_t nnz) {
     return m;
 }
 
+namespace {
+constexpr size_t BIG_BYTES = size_t(256) << 20;
+constexpr size_t BIG_ROUND = size_t(64) << 20;
+constexpr size_t BIG_KEEP = 6;  // cached blocks per context
+
+// Best-fit block of at least `bytes` (at most 2x larger) from the context's
+// cache, else a fresh pool block rounded up to 64 MB. Stream order on the
+// context stream makes reuse safe (the block was freed on the same stream).
+void* big_alloc(spg_ctx* ctx, size_t bytes, size_t* cap) {
+    int best = -1;
+    for (size_t i = 0; i < ctx->big_cache.size(); ++i) {
+        const size_t sz = ctx->big_cache[i].second;
+        if (sz >= bytes && sz <= 2 * bytes + BIG_ROUND && (best < 0 || sz < ctx->big_cache[best].second))
+            best = static_cast<int>(i);
+    }
+    if (best >= 0) {
+        void* p = ctx->big_cache[best].first;
+        *cap = ctx->big_cache[best].second;
+        ctx->big_cache.erase(ctx->big_cache.begin() + best);
+        return p;
+    }
+    const size_t sz = (bytes + BIG_ROUND - 1) / BIG_ROUND * BIG_ROUND;
+    void* p = nullptr;
+    SPG_CUDA(cudaMallocFromPoolAsync(&p, sz, ctx->pool, ctx->stream));
+    *cap = sz;
+    return p;
+}
+
+void big_free(spg_ctx* ctx, void* p, size_t cap) {
+    ctx->big_cache.emplace_back(p, cap);
+    if (ctx->big_cache.size() > BIG_KEEP) {  // drop the smallest
+        size_t k = 0;
+        for (size_t i = 1; i < ctx->big_cache.size(); ++i)
+            if (ctx->big_cache[i].second < ctx->big_cache[k].second) k = i;
+        cudaFreeAsync(ctx->big_cache[k].first, ctx->stream);
+        ctx->big_cache.erase(ctx->big_cache.begin() + k);
+    }
+}
+}  // namespace
+
+void alloc_c_arrays(spg_ctx* ctx, spg_csr* c, int64_t cap) {
+    const size_t n = static_cast<size_t>(cap > 0 ? cap : 1);
+    if (n * sizeof(int32_t) >= BIG_BYTES) {
+        c->colind = static_cast<int32_t*>(big_alloc(ctx, n * sizeof(int32_t), &c->big_col));
+        c->values = static_cast<double*>(big_alloc(ctx, n * sizeof(double), &c->big_val));
+    } else {
+        c->colind = dalloc<int32_t>(ctx, n);
+        c->values = dalloc<double>(ctx, n);
+    }
+}
+
+void big_cache_release(spg_ctx* ctx) {
+    for (auto& b : ctx->big_cache) cudaFreeAsync(b.first, ctx->stream);
+    ctx->big_cache.clear();
+}
+
 void free_csr(spg_csr* m) {
     if (!m) return;
     DeviceScope ds(m->ctx->device);
     if (m->storage == 0) {
         dfree(m->ctx, m->rowptr);
-        dfree(m->ctx, m->colind);
-        dfree(m->ctx, m->values);
+        if (m->big_col) big_free(m->ctx, m->colind, m->big_col);
+        else dfree(m->ctx, m->colind);
+        if (m->big_val) big_free(m->ctx, m->values, m->big_val);
+        else dfree(m->ctx, m->values);
     } else if (m->storage == 1) {
         cudaStreamSynchronize(m->ctx->stream);
         cudaFree(m->rowptr);
@@ -331,8 +389,7 @@ spg_csr* spgeam(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     }
     exclusive_scan_i64(ctx, cnt, c->rowptr, m);
     c->nnz = read_scalar(ctx, c->rowptr + m);
-    c->colind = dalloc<int32_t>(ctx, c->nnz);
-    c->values = dalloc<double>(ctx, c->nnz);
+    alloc_c_arrays(ctx, c, c->nnz);
     {
         KTime kt(ctx, "spgeam_write");
         k_spgeam<true><<<g, 256, 0, ctx->stream>>>(a->rowptr, a->colind, a->values, b->rowptr, b->colind, b->values,
@@ -416,8 +473,7 @@ spg_csr* extract(spg_ctx* ctx, const spg_csr* m, int64_t r0, int64_t r1, int64_t
     SPG_LAUNCH_CHECK();
     exclusive_scan_i64(ctx, cnt, t->rowptr, rows);
     t->nnz = read_scalar(ctx, t->rowptr + rows);
-    t->colind = dalloc<int32_t>(ctx, t->nnz);
-    t->values = dalloc<double>(ctx, t->nnz);
+    alloc_c_arrays(ctx, t, t->nnz);
     k_extract_copy<<<grid_for(ctx, rows * 32), 256, 0, ctx->stream>>>(beg, t->rowptr, rows, m->colind, m->values, c0,
                                                                       t->colind, t->values);
     SPG_LAUNCH_CHECK();
@@ -459,8 +515,7 @@ spg_csr* prune(spg_ctx* ctx, const spg_csr* a, double th) {
     }
     exclusive_scan_i64(ctx, cnt, r->rowptr, m);
     r->nnz = read_scalar(ctx, r->rowptr + m);
-    r->colind = dalloc<int32_t>(ctx, r->nnz);
-    r->values = dalloc<double>(ctx, r->nnz);
+    alloc_c_arrays(ctx, r, r->nnz);
     if (m) {
         k_prune_copy<<<grid_for(ctx, m * 32), 256, 0, ctx->stream>>>(a->rowptr, a->colind, a->values, m, th, r->rowptr,
                                                                      r->colind, r->values);

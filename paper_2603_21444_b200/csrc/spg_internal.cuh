@@ -66,6 +66,10 @@ struct spg_ctx {
     // Pinned host staging for small scalar read-backs.
     int64_t* host_scalars = nullptr;
     bool tile_attr_set = false;
+    // Large C arrays (>= 256 MB) come from this block cache instead of the pool:
+    // the pool splits freed blocks for smaller requests, after which a
+    // multi-GB request maps fresh memory on every call (see big_alloc).
+    std::vector<std::pair<void*, size_t>> big_cache;
     int two_pass = 0;  // 1: symbolic + numeric warp kernels instead of the single-pass tiles (SPG_TWO_PASS=1)
 };
 
@@ -78,6 +82,7 @@ struct spg_csr {
     // Storage kind: 0 = stream-ordered pool (default), 1 = cudaMalloc (IPC
     // exportable), 2 = IPC view of a peer process's matrix (read-only).
     int storage = 0;
+    size_t big_col = 0, big_val = 0;  // capacities (bytes) of colind/values taken from ctx->big_cache
 };
 
 namespace spgb {
@@ -142,6 +147,9 @@ struct KTime {
 
 spg_csr* new_csr(spg_ctx* ctx, int64_t nrows, int64_t ncols, int64_t nnz);
 void free_csr(spg_csr* m);
+// colind/values of a new product with room for `cap` entries (big arrays via the block cache).
+void alloc_c_arrays(spg_ctx* ctx, spg_csr* c, int64_t cap);
+void big_cache_release(spg_ctx* ctx);
 int64_t read_scalar(spg_ctx* ctx, const int64_t* dptr);
 
 // Kernels (spgemm.cu / spgeam.cu / misc.cu)

@@ -25,7 +25,10 @@
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <chrono>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 
 #include "block_scan.cuh"
 #include "spg_internal.cuh"
@@ -1625,8 +1628,7 @@ spg_csr* spgemm_two_pass(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     spg_csr* c = new_csr(ctx, m, n, -1);
     exclusive_scan_i64(ctx, rnnz, c->rowptr, m);
     c->nnz = read_scalar(ctx, c->rowptr + m);
-    c->colind = dalloc<int32_t>(ctx, c->nnz);
-    c->values = dalloc<double>(ctx, c->nnz);
+    alloc_c_arrays(ctx, c, c->nnz);
     {
         KTime kt(ctx, "spgemm_numeric");
         {
@@ -1646,8 +1648,25 @@ spg_csr* spgemm_two_pass(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     return c;
 }
 
+// Host-side phase timer (SPG_HOST_PROF=1 prints one line per multiply).
+struct HostProf {
+    bool on = std::getenv("SPG_HOST_PROF") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+    std::string out;
+    void mark(const char* what) {
+        if (!on) return;
+        const auto t = std::chrono::steady_clock::now();
+        out += std::string(what) + "=" + std::to_string(std::chrono::duration<double, std::milli>(t - last).count()) + " ";
+        last = t;
+    }
+    ~HostProf() {
+        if (on) std::fprintf(stderr, "[spgemm host ms] %s\n", out.c_str());
+    }
+};
+
 // Single-pass tiled multiply (the default).
 spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
+    HostProf hp;
     const int64_t m = a->nrows, n = b->ncols;
     const int cshift = cshift_for(n);
     // 1: products, entry spans, row weights, BIG-row lists
@@ -1657,6 +1676,7 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     int32_t* cta_list = lists.get();
     int32_t* heavy_list = lists.get() + m;
     SPG_CUDA(cudaMemsetAsync(counts.get(), 0, 2 * sizeof(int32_t), ctx->stream));
+    hp.mark("alloc1");
     {
         KTime kt(ctx, "row_prep");
         k_row_prep<<<grid_for(ctx, 32 * m), 256, 0, ctx->stream>>>(a->rowptr, a->colind, b->rowptr, m, prod, wt,
@@ -1681,7 +1701,9 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
         k_tile_flags<<<grid_for(ctx, m), 256, 0, ctx->stream>>>(wpre, prod, a->rowptr, m, flag);
         SPG_LAUNCH_CHECK();
     }
+    hp.mark("launch1");
     SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+    hp.mark("sync1");
     const int ncta = hc[0], nheavy = hc[1], nside = ncta + nheavy;
 
     // 3: BIG rows into a side buffer (symbolic, offsets, numeric)
@@ -1763,9 +1785,11 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
                                                           side_off, s_col, s_val);
         SPG_LAUNCH_CHECK();
     }
+    hp.mark("side");
     // 4: tiles
     exclusive_scan_i64(ctx, flag, fpos, m);
     const int64_t ntiles = read_scalar(ctx, fpos.get() + m);
+    hp.mark("tilescan");
     DBuf<int64_t> tr(ctx, ntiles + 1), te(ctx, ntiles + 1);
     DBuf<uint64_t> status(ctx, ntiles);
     {
@@ -1778,8 +1802,9 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     DBuf<unsigned long long> ticket(ctx, 1);
     SPG_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned long long), ctx->stream));
     spg_csr* c = new_csr(ctx, m, n, -1);
-    c->colind = dalloc<int32_t>(ctx, products);  // upper bound of nnz(C)
-    c->values = dalloc<double>(ctx, products);
+    hp.mark("tilesetup");
+    alloc_c_arrays(ctx, c, products);  // upper bound of nnz(C)
+    hp.mark("allocC");
     SPG_CUDA(cudaMemsetAsync(c->rowptr, 0, sizeof(int64_t), ctx->stream));
     int occ = 1;
     SPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile, tile::NT, sizeof(TileSmem)));
@@ -1791,7 +1816,9 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
                                                                   s_val, status, c->rowptr, c->colind, c->values);
         SPG_LAUNCH_CHECK();
     }
+    hp.mark("launch_tile");
     c->nnz = read_scalar(ctx, c->rowptr + m);
+    hp.mark("tile");
     return c;
 }
 }  // namespace

@@ -141,6 +141,7 @@ spg_csr* run_rank(spg_ctx* ctx, const std::vector<RoundPlan>& plan, const spg_cs
     SPG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     spg_ctx cctx = *ctx;  // same device and pool, copy stream
     cctx.stream = cs;
+    cctx.big_cache.clear();  // the block cache belongs to ctx (its stream orders reuse)
     cctx.timer = Timer{};
     const int R = static_cast<int>(plan.size());
     std::vector<spg_csr*> a_in(R, nullptr), b_in(R, nullptr);
