@@ -396,6 +396,54 @@ def ours_multi(args):
     launches = sum(v[0] for v in kt.values())
     lt = torch.tensor([launches], dtype=torch.int64, device=f"cuda:{local}")
     dist.all_reduce(lt)
+    # end to end through the public API with HOST buffers: every step each rank
+    # refills its tiles from pinned host memory (H2D), the ranks run the trident
+    # step (peer pulls over NVLink), and each rank downloads its C tile (D2H)
+    from paper_2603_21444_b200 import _capi
+    L = _capi.lib()
+
+    def host_arrays(m):
+        arrs = (np.ascontiguousarray(m.rowptr, np.int64), np.ascontiguousarray(np.asarray(m.colind), np.int32),
+                np.ascontiguousarray(m.values, np.float64))
+        for x in arrs:
+            _capi.check(L.spg_host_register(x.ctypes.data, max(x.nbytes, 1)))
+        return arrs
+
+    at_h, bt_h = host_arrays(at), host_arrays(bt)
+    m_c = int(at.nrows)
+    c_rp = np.empty(m_c + 1, np.int64)
+    c_ci = np.empty(max(nnz_c, 1), np.int32)
+    c_va = np.empty(max(nnz_c, 1), np.float64)
+    for x in (c_rp, c_ci, c_va):
+        _capi.check(L.spg_host_register(x.ctypes.data, x.nbytes))
+
+    def e2e_step():
+        ex.reload(at_h, bt_h)
+        dist.barrier()
+        c, _ = ex.trident_step(procs, lam, grid.q)
+        _capi.check(L.spg_csr_download(dev.ctx, c.h, c_rp.ctypes.data, c_ci.ctypes.data, 4, c_va.ctypes.data))
+        c.free()
+
+    e2e_steps = max(1, min(args.steps, int(os.environ.get("SPG_E2E_STEPS", 3))))
+    e2e_step()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    dev.synchronize()
+    e2e_local = (time.perf_counter() - t0) / e2e_steps * 1e3
+    et = torch.tensor([e2e_local], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_ms = float(et.item())
+    h2d = sum(x.nbytes for x in at_h + bt_h)
+    d2h = c_rp.nbytes + nnz_c * 12
+    hb = torch.tensor([h2d, d2h], dtype=torch.int64, device=f"cuda:{local}")
+    dist.all_reduce(hb)
+    for x in at_h + bt_h + (c_rp, c_ci, c_va):
+        L.spg_host_unregister(x.ctypes.data)
+    # roofline of rank 0's multiply kernel: its algorithmic bytes / its time
+    prod0 = sd.rank_products(a, a, grid, 0) if rank == 0 else 0
+
     ledger = sd.ledger_for(a, a, grid)
     recv_bytes = int(ledger[:, 1, :, 2].sum(axis=1).max())
     tl_mean = np.mean(np.stack(tls), axis=0)  # [q, 4] ms
@@ -408,6 +456,14 @@ def ours_multi(args):
         peak, peak_kind = measured_peaks()
         gflops = 2.0 * products_total / (ms * 1e-3) / 1e9
         num = kt.get("spgemm_tile", kt.get("spgemm_numeric", (1, 0.0)))
+        kms = num[1] / max(1, num[0])
+        # rank 0's multiply: A tile rows/nnz, gathers of its products, its C tile
+        ba0 = alg_bytes(int(at.nrows), int(at.nnz) * grid.q, prod0, nnz_c)
+        ach = ba0 / (kms * 1e-3) / 1e9 if kms > 0 else None
+        roof0 = {"bound": "hbm", "kernel": "k_tile (rank 0, its trident rounds)", "peak": peak, "unit": "GB/s",
+                 "achieved": round(ach, 1) if ach else None, "frac": round(ach / peak, 4) if ach else None,
+                 "traffic": None, "algorithmic_bytes": ba0, "kernel_ms": round(kms, 4), "products_rank0": prod0,
+                 "peak_kind": peak_kind}
         line = {
             "metric": METRIC, "value": round(gflops, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
@@ -420,8 +476,12 @@ def ours_multi(args):
             "exchange": {"ledger_max_recv_bytes_per_rank": recv_bytes, "exchange_ms_rank0": round(exch_ms, 4),
                          "nvlink_frac_rank0": round(recv_bytes / max(exch_ms, 1e-9) / 1e6 / 770.0, 4),
                          "nvlink_peak_gbs": 770.0},
-            "roofline": {"bound": "hbm", "kernel": "k_tile (rank 0)", "peak": peak, "unit": "GB/s",
-                         "achieved": None, "frac": None, "traffic": None, "peak_kind": peak_kind},
+            "roofline": roof0,
+            "e2e": {"value": round(2.0 * products_total / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+                    "ms_per_step": round(e2e_ms, 2), "h2d_bytes_per_step": int(hb[0].item()),
+                    "d2h_bytes_per_step": int(hb[1].item()),
+                    "path": "per rank: spg_csr_upload_into (pinned host -> its tiles), spg_trident_rank, "
+                            "spg_csr_download of its C tile; max over ranks"},
             "clocks": clk.summary(),
             "gpu_launches": int(lt.item()),
         }

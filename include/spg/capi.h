@@ -86,6 +86,11 @@ spg_status spg_csr_zeros(spg_ctx* ctx, int64_t nrows, int64_t ncols, spg_csr** o
 spg_status spg_csr_shape(const spg_csr* m, int64_t* nrows, int64_t* ncols, int64_t* nnz);
 /* Download into caller-allocated arrays sized from spg_csr_shape. Any pointer
  * may be NULL to skip that array. colind_width 4 or 8. */
+/* Refills an existing device matrix from host arrays of the SAME shape and nnz
+ * (int32 colind), keeping its device buffers (and any IPC export) in place.
+ * The end-to-end benchmark's per-step upload of resident tiles. */
+spg_status spg_csr_upload_into(spg_ctx* ctx, spg_csr* m, const int64_t* rowptr, const int32_t* colind,
+                               const double* values);
 spg_status spg_csr_download(spg_ctx* ctx, const spg_csr* m, int64_t* rowptr, void* colind, int colind_width,
                             double* values);
 /* Device-side canonical check (csr.cpp:30-50): SPG_OK or SPG_ERROR with a

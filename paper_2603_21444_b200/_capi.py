@@ -17,7 +17,7 @@ CXX_LIB_PATH = os.path.join(_HERE, "lib", "libspgsim_b200.so")
 EXPORTS = [
     "spg_last_error", "spg_version", "spg_device_count", "spg_init", "spg_finalize", "spg_ctx_stream", "spg_ctx_synchronize",
     "spg_ctx_device", "spg_timing_enable", "spg_timing_reset", "spg_timing_read", "spg_csr_upload",
-    "spg_csr_zeros", "spg_csr_shape", "spg_csr_download", "spg_csr_check", "spg_csr_free",
+    "spg_csr_zeros", "spg_csr_shape", "spg_csr_upload_into", "spg_csr_download", "spg_csr_check", "spg_csr_free",
     "spg_csr_device_ptrs", "spg_spgemm", "spg_spgemm_products", "spg_spgeam", "spg_spgeam_inplace",
     "spg_vconcat", "spg_csr_extract", "spg_csr_copy", "spg_spgemm_host", "spg_column_normalize", "spg_prune",
     "spg_trident_grid", "spg_trident_spgemm", "spg_summa_spgemm",
@@ -65,6 +65,7 @@ def lib() -> C.CDLL:
         "spg_csr_upload": (st, [vp, i64, i64, vp, vp, i32, vp, P(vp)]),
         "spg_csr_zeros": (st, [vp, i64, i64, P(vp)]),
         "spg_csr_shape": (st, [vp, P(i64), P(i64), P(i64)]),
+        "spg_csr_upload_into": (st, [vp, vp, vp, vp, vp]),
         "spg_csr_download": (st, [vp, vp, vp, vp, i32, vp]),
         "spg_csr_check": (st, [vp, vp]),
         "spg_csr_free": (st, [vp]),

@@ -248,6 +248,23 @@ spg_status spg_csr_shape(const spg_csr* m, int64_t* nrows, int64_t* ncols, int64
     });
 }
 
+spg_status spg_csr_upload_into(spg_ctx* ctx, spg_csr* m, const int64_t* rowptr, const int32_t* colind,
+                               const double* values) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(m, "m");
+        if (m->storage == 2) fail(SPG_PARAMETER_ERROR, "spg_csr_upload_into: read-only IPC view");
+        DeviceScope ds(m->ctx->device);
+        cudaStream_t st = m->ctx->stream;
+        SPG_CUDA(cudaMemcpyAsync(m->rowptr, rowptr, (m->nrows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        if (m->nnz) {
+            SPG_CUDA(cudaMemcpyAsync(m->colind, colind, m->nnz * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+            SPG_CUDA(cudaMemcpyAsync(m->values, values, m->nnz * sizeof(double), cudaMemcpyHostToDevice, st));
+        }
+        SPG_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
 spg_status spg_csr_download(spg_ctx* ctx, const spg_csr* m, int64_t* rowptr, void* colind, int colind_width,
                             double* values) {
     return guard([&] {

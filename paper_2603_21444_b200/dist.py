@@ -88,6 +88,13 @@ class RankExchange:
         check(L.spg_trident_rank(self.dev.ctx, self.rank, procs, gpus_per_node, va, vb, C.byref(out), tl))
         return DeviceCsr(self.dev, out.value), np.ctypeslib.as_array(tl).reshape(q, 4).copy()
 
+    def reload(self, a_host, b_host):
+        """Refill this rank's shareable A/B tiles from host arrays (pinned by
+        the caller) in place, so the peers' IPC views stay valid (e2e leg)."""
+        L = _capi.lib()
+        for d, m in zip(self.own, (a_host, b_host)):
+            check(L.spg_csr_upload_into(self.dev.ctx, d.h, m[0].ctypes.data, m[1].ctypes.data, m[2].ctypes.data))
+
     def close(self):
         for lst in (self.views_a, self.views_b):
             for i, v in enumerate(lst):
@@ -97,9 +104,33 @@ class RankExchange:
             d.free()
 
 
+def rank_products(a, b, grid: TridentGrid, rank: int) -> int:
+    """Products of all of this rank's local multiplies (sum over its q rounds
+    of products(A_{i,s,k}, B_{s,j})), from the global matrices (host numpy)."""
+    q, lam = grid.q, grid.gpus_per_node
+    i, j, k = grid.coords_of(rank)
+    tm_a = make_tile_map(int(a.nrows), int(a.ncols), "trident", grid.procs, lam)
+    tm_b = make_tile_map(int(b.nrows), int(b.ncols), "trident", grid.procs, lam)
+    cb = np.asarray(tm_b.col_bounds, np.int64)
+    brp, bci = np.asarray(b.rowptr, np.int64), np.asarray(b.colind, np.int64)
+    brow = np.repeat(np.arange(int(b.nrows)), np.diff(brp))
+    lo, hi = cb[j], cb[j + 1]
+    keep = (bci >= lo) & (bci < hi)
+    blen = np.bincount(brow[keep], minlength=int(b.nrows))  # nnz of B rows inside column block j
+    total = 0
+    for r in range(q):
+        s = (r + i + j) % q
+        r0, r1, c0, c1 = tm_a.tiles[grid.rank_of(i, s, k)]
+        arp, aci = np.asarray(a.rowptr, np.int64), np.asarray(a.colind, np.int64)
+        cols = aci[int(arp[r0]):int(arp[r1])]
+        cols = cols[(cols >= c0) & (cols < c1)]
+        total += int(blen[cols].sum())
+    return total
+
+
 def ledger_for(a, b, grid: TridentGrid, iw: int = 4, vw: int = 8) -> np.ndarray:
     sa, sb = all_shapes(a, b, grid)
     return trident_ledger(grid, sa, sb, iw, vw)
 
 
-__all__ = ["grid_for_gpus", "rank_tiles", "all_shapes", "RankExchange", "ledger_for", "CsrMatrix"]
+__all__ = ["grid_for_gpus", "rank_tiles", "all_shapes", "rank_products", "RankExchange", "ledger_for", "CsrMatrix"]

@@ -1,2 +1,2 @@
-nvidia-smi --query-gpu=index,name --format=csv
-SPG_HOST_PROF=1 SPG_BENCH_DEBUG=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 5 --warmup 3 > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err; tail -c 2500 gpurun_out/bench_n2.json; grep "rank\|host ms" gpurun_out/bench_n2.err | tail -12
+N=${N:-2}
+SPG_BENCH_DEBUG=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus $N --steps 5 --warmup 3 > gpurun_out/bench_n$N.json 2> gpurun_out/bench_n$N.err; tail -c 3000 gpurun_out/bench_n$N.json; grep "rank\|Error\|error" gpurun_out/bench_n$N.err | tail -12
