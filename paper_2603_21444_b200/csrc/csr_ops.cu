@@ -178,18 +178,18 @@ __global__ void k_extract_copy(const int64_t* __restrict__ beg, const int64_t* _
 
 // ------------------------------------------------------- column_normalize
 // Column sums in CSR storage order (reference csr.cpp:225-227): entries are
-// stably radix-sorted by column (storage index as payload), then each column is
-// summed sequentially in storage order, so sums are bit-identical.
+// stably radix-sorted by column (value as payload), then each column is summed
+// sequentially in storage order, so sums are bit-identical.
 __global__ void k_iota_i64(int64_t* p, int64_t n) { GRID_STRIDE(i, n) p[i] = i; }
 
-__global__ void k_colsum_sorted(const int32_t* __restrict__ keys, const int64_t* __restrict__ idx, int64_t nnz,
-                                const double* __restrict__ val, double* __restrict__ colsum) {
-    // one thread per run start
+__global__ void k_colsum_runs(const int32_t* __restrict__ keys, const double* __restrict__ sval, int64_t nnz,
+                              double* __restrict__ colsum) {
+    // one thread per run start (a run = one column, values in storage order)
     GRID_STRIDE(t, nnz) {
         if (t > 0 && keys[t - 1] == keys[t]) continue;
         const int32_t c = keys[t];
         double s = 0.0;
-        for (int64_t u = t; u < nnz && keys[u] == c; ++u) s = __dadd_rn(s, val[idx[u]]);
+        for (int64_t u = t; u < nnz && keys[u] == c; ++u) s = __dadd_rn(s, sval[u]);
         colsum[c] = s;
     }
 }
@@ -290,9 +290,9 @@ spg_csr* new_csr(spg_ctx* ctx, int64_t nrows, int64_t ncols, int64_t nnz) {
 }
 
 namespace {
-constexpr size_t BIG_BYTES = size_t(256) << 20;
 constexpr size_t BIG_ROUND = size_t(64) << 20;
-constexpr size_t BIG_KEEP = 6;  // cached blocks per context
+constexpr size_t BIG_KEEP = 16;  // cached blocks per context
+}  // namespace
 
 // Best-fit block of at least `bytes` (at most 2x larger) from the context's
 // cache, else a fresh pool block rounded up to 64 MB. Stream order on the
@@ -327,7 +327,6 @@ void big_free(spg_ctx* ctx, void* p, size_t cap) {
         ctx->big_cache.erase(ctx->big_cache.begin() + k);
     }
 }
-}  // namespace
 
 void alloc_c_arrays(spg_ctx* ctx, spg_csr* c, int64_t cap) {
     const size_t n = static_cast<size_t>(cap > 0 ? cap : 1);
@@ -484,21 +483,23 @@ void column_normalize(spg_ctx* ctx, spg_csr* m) {
     const int64_t nnz = m->nnz;
     if (nnz == 0) return;
     if (nnz > INT32_MAX) fail(SPG_PARAMETER_ERROR, "column_normalize: nnz exceeds 2^31");
+    // stable radix sort of (column -> value): each column's values end up
+    // contiguous in storage (row) order, then one thread per column sums them
+    // sequentially like the reference loop (csr.cpp:225-227)
     DBuf<int32_t> keys(ctx, nnz);
-    DBuf<int64_t> idx(ctx, nnz), idx_sorted(ctx, nnz);
+    DBuf<double> vals(ctx, nnz);
     DBuf<double> colsum(ctx, m->ncols);
     KTime kt(ctx, "column_normalize");
-    k_iota_i64<<<grid_for(ctx, nnz), 256, 0, ctx->stream>>>(idx, nnz);
     int bits = 1;
     while ((int64_t(1) << bits) < m->ncols) ++bits;
     size_t tmp = 0;
-    SPG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, m->colind, keys.get(), idx.get(), idx_sorted.get(),
+    SPG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, m->colind, keys.get(), m->values, vals.get(),
                                              static_cast<int>(nnz), 0, bits, ctx->stream));
     DBuf<unsigned char> t(ctx, tmp);
-    SPG_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, m->colind, keys.get(), idx.get(), idx_sorted.get(),
+    SPG_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, m->colind, keys.get(), m->values, vals.get(),
                                              static_cast<int>(nnz), 0, bits, ctx->stream));
     SPG_CUDA(cudaMemsetAsync(colsum.get(), 0, m->ncols * sizeof(double), ctx->stream));
-    k_colsum_sorted<<<grid_for(ctx, nnz), 256, 0, ctx->stream>>>(keys, idx_sorted, nnz, m->values, colsum);
+    k_colsum_runs<<<grid_for(ctx, nnz), 256, 0, ctx->stream>>>(keys, vals, nnz, colsum);
     k_scale_cols<<<grid_for(ctx, nnz), 256, 0, ctx->stream>>>(m->colind, m->values, nnz, colsum);
     SPG_LAUNCH_CHECK();
 }

@@ -111,14 +111,24 @@ inline void dfree(spg_ctx* ctx, void* p) {
     if (p) cudaFreeAsync(p, ctx->stream);
 }
 
-// Stream-ordered scratch buffer freed at scope exit.
+void* big_alloc(spg_ctx* ctx, size_t bytes, size_t* cap);
+void big_free(spg_ctx* ctx, void* p, size_t cap);
+constexpr size_t BIG_BYTES = size_t(256) << 20;
+
+// Stream-ordered scratch buffer freed at scope exit (>= 256 MB: block cache).
 template <class T>
 struct DBuf {
     spg_ctx* ctx;
     T* p = nullptr;
-    size_t n = 0;
-    DBuf(spg_ctx* c, size_t count) : ctx(c), n(count) { p = dalloc<T>(c, count); }
-    ~DBuf() { dfree(ctx, p); }
+    size_t n = 0, cap = 0;
+    DBuf(spg_ctx* c, size_t count) : ctx(c), n(count) {
+        if (count * sizeof(T) >= BIG_BYTES) p = static_cast<T*>(big_alloc(c, count * sizeof(T), &cap));
+        else p = dalloc<T>(c, count);
+    }
+    ~DBuf() {
+        if (cap) big_free(ctx, p, cap);
+        else dfree(ctx, p);
+    }
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
     T* get() const { return p; }

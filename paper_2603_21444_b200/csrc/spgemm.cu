@@ -843,11 +843,17 @@ constexpr int NJ = (PMAX + NT - 1) / NT;        // product slots per thread
 constexpr int EPT = (EMAX + NT - 1) / NT;       // entry slots per thread
 constexpr int HW = PMAX / 32 + 2;               // words of the head bitmap
 constexpr int LMAX = PMAX / 3 + 1;              // shared buckets of >= 3 products
-// espan[e] of an entry of a tile row: B row start (34 bits) | B row length (10)
-// | product offset of the entry in its row (10) | products of the row (10)
-constexpr int SP_BS = 34, SP_LEN = 34, SP_IN = 44, SP_PR = 54;
+// espan[e] of an entry of a tile row: B row start (30 bits) | B row length (10)
+// | product offset of the entry in its row (12) | products of the row (12)
+constexpr int SP_BS = 30, SP_LEN = 30, SP_IN = 40, SP_PR = 52;
+constexpr int SP_LEN_MAX = 1023;
 constexpr uint64_t SP_BS_MASK = (uint64_t(1) << SP_BS) - 1;
 }  // namespace tile
+
+// Row kinds: SMALL rows share windowed tiles; a MEDIUM row (not small, but
+// products + 4*entries + 4 <= PMAX and every B row it reads <= SP_LEN_MAX
+// long) is a tile of its own; BIG rows go to the side path.
+enum : int8_t { RK_SMALL = 0, RK_MEDIUM = 1, RK_BIG = 2 };
 
 // Row weight: tiles are runs of small rows within one TW-window of the
 // exclusive prefix of weights, so a tile has < PMAX products, < PMAX/4
@@ -858,36 +864,22 @@ __host__ __device__ __forceinline__ bool tile_small(int64_t p, int64_t ne) {
 }
 
 // Per row (warp per row, lanes over entries): products(i) = Σ nnz(B_k), the
-// packed entry spans of tile rows (so the tile kernel reads its entries with no
-// dependent B.rowptr load and no row pass), the row weight, and the BIG-row
-// lists: 0 = CTA rows (<= CTA_P products, <= CTA_E entries), 1 = heavy.
+// row kind, the packed entry spans of tile rows (so the tile kernel reads its
+// entries with no dependent B.rowptr load and no row pass), the row weight,
+// and the BIG-row lists: 0 = CTA rows (<= CTA_P products, <= CTA_E entries),
+// 1 = heavy.
 __global__ void k_row_prep(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
                            const int64_t* __restrict__ brp, int64_t m, int64_t* __restrict__ prod,
-                           int64_t* __restrict__ wt, uint64_t* __restrict__ espan, int32_t* __restrict__ lists,
-                           int32_t* __restrict__ counts) {
+                           int64_t* __restrict__ wt, int8_t* __restrict__ kind, uint64_t* __restrict__ espan,
+                           int32_t* __restrict__ lists, int32_t* __restrict__ counts) {
     const int lane = threadIdx.x & 31;
     const int64_t gw = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
     const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
     for (int64_t i = gw; i < m; i += nw) {
         const int64_t e0 = arp[i], e1 = arp[i + 1];
-        int64_t p = 0;
-        int64_t bsv[2] = {0, 0};
-        int lenv[2] = {0, 0}, inv[2] = {0, 0};
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {  // the first 64 entries (all of a tile row's)
-            const int64_t e = e0 + 32 * c + lane;
-            int64_t len = 0;
-            if (e < e1) {
-                const int32_t k = __ldg(acol + e);
-                bsv[c] = __ldg(brp + k);
-                len = __ldg(brp + k + 1) - bsv[c];
-            }
-            const int64_t inc = warp_inclusive_scan(len);
-            inv[c] = static_cast<int>(min(p + inc - len, int64_t(1023)));
-            lenv[c] = static_cast<int>(min(len, int64_t(1023)));
-            p += __shfl_sync(0xffffffffu, inc, 31);
-        }
-        for (int64_t eb = e0 + 64; eb < e1; eb += 32) {  // BIG rows only (> 64 entries)
+        const int64_t ne = e1 - e0;
+        int64_t p = 0, maxlen = 0;
+        for (int64_t eb = e0; eb < e1; eb += 32) {  // warp-uniform trip count
             const int64_t e = eb + lane;
             int64_t len = 0;
             if (e < e1) {
@@ -895,24 +887,37 @@ __global__ void k_row_prep(const int64_t* __restrict__ arp, const int32_t* __res
                 len = __ldg(brp + k + 1) - __ldg(brp + k);
             }
             p += warp_reduce_sum(len);
+            maxlen = max(maxlen, len);
         }
-        const int64_t ne = e1 - e0;
-        const bool small = tile_small(p, ne);
-        if (small) {
-            const uint64_t pr = static_cast<uint64_t>(p);
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const int64_t e = e0 + 32 * c + lane;
+        for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+        int8_t rk = RK_BIG;
+        if (tile_small(p, ne)) rk = RK_SMALL;
+        else if (tile_weight(p, ne) <= tile::PMAX && maxlen <= tile::SP_LEN_MAX) rk = RK_MEDIUM;
+        if (rk != RK_BIG) {  // second pass: in-row product offsets -> espan
+            const uint64_t pr = static_cast<uint64_t>(p);
+            int64_t carry = 0;
+            for (int64_t eb = e0; eb < e1; eb += 32) {
+                const int64_t e = eb + lane;
+                int64_t bs = 0, len = 0;
+                if (e < e1) {
+                    const int32_t k = __ldg(acol + e);
+                    bs = __ldg(brp + k);
+                    len = __ldg(brp + k + 1) - bs;
+                }
+                const int64_t inc = warp_inclusive_scan(len);
                 if (e < e1)
-                    espan[e] = (static_cast<uint64_t>(bsv[c]) & tile::SP_BS_MASK) |
-                               (static_cast<uint64_t>(lenv[c]) << tile::SP_LEN) |
-                               (static_cast<uint64_t>(inv[c]) << tile::SP_IN) | (pr << tile::SP_PR);
+                    espan[e] = (static_cast<uint64_t>(bs) & tile::SP_BS_MASK) |
+                               (static_cast<uint64_t>(len) << tile::SP_LEN) |
+                               (static_cast<uint64_t>(carry + inc - len) << tile::SP_IN) | (pr << tile::SP_PR);
+                carry += __shfl_sync(0xffffffffu, inc, 31);
             }
         }
         if (lane == 0) {
             prod[i] = p;
-            wt[i] = small ? tile_weight(p, ne) : 0;
-            if (!small) {
+            kind[i] = rk;
+            wt[i] = rk == RK_SMALL ? tile_weight(p, ne) : 0;
+            if (rk == RK_BIG) {
                 const int c = (ne <= CTA_E && p <= CTA_P) ? 0 : 1;
                 lists[c * m + atomicAdd(counts + c, 1)] = static_cast<int32_t>(i);
             }
@@ -920,17 +925,14 @@ __global__ void k_row_prep(const int64_t* __restrict__ arp, const int32_t* __res
     }
 }
 
-// Tile starts: row i starts a tile if it is BIG, follows a BIG row, or its
-// weight prefix enters a new TW-window.
-__global__ void k_tile_flags(const int64_t* __restrict__ wpre, const int64_t* __restrict__ prod,
-                             const int64_t* __restrict__ arp, int64_t m, int64_t* __restrict__ flag) {
+// Tile starts: row i starts a tile if it is not SMALL, follows a row that is
+// not SMALL, or its weight prefix enters a new TW-window.
+__global__ void k_tile_flags(const int64_t* __restrict__ wpre, const int8_t* __restrict__ kind, int64_t m,
+                             int64_t* __restrict__ flag) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
-        const bool big = !tile_small(prod[i], arp[i + 1] - arp[i]);
         int f = 1;
-        if (i > 0 && !big) {
-            const bool prev_big = !tile_small(prod[i - 1], arp[i] - arp[i - 1]);
-            f = prev_big || (wpre[i] / tile::TW != wpre[i - 1] / tile::TW);
-        }
+        if (i > 0 && kind[i] == RK_SMALL)
+            f = kind[i - 1] != RK_SMALL || (wpre[i] / tile::TW != wpre[i - 1] / tile::TW);
         flag[i] = f;
     }
 }
@@ -938,7 +940,7 @@ __global__ void k_tile_flags(const int64_t* __restrict__ wpre, const int64_t* __
 // Compacts the tile starts: tr[t] = first row | BIG flag (bit 62), te[t] = its
 // first entry; tr[ntiles] = m, te[ntiles] = nnz(A).
 __global__ void k_tile_scatter(const int64_t* __restrict__ flag, const int64_t* __restrict__ fpos,
-                               const int64_t* __restrict__ prod, const int64_t* __restrict__ arp, int64_t m,
+                               const int8_t* __restrict__ kind, const int64_t* __restrict__ arp, int64_t m,
                                int64_t* __restrict__ tr, int64_t* __restrict__ te) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i <= m; i += int64_t(gridDim.x) * blockDim.x) {
         if (i == m) {
@@ -946,8 +948,7 @@ __global__ void k_tile_scatter(const int64_t* __restrict__ flag, const int64_t* 
             tr[nt] = m;
             te[nt] = arp[m];
         } else if (flag[i]) {
-            const bool big = !tile_small(prod[i], arp[i + 1] - arp[i]);
-            tr[fpos[i]] = i | (big ? (int64_t(1) << 62) : 0);
+            tr[fpos[i]] = i | (kind[i] == RK_BIG ? (int64_t(1) << 62) : 0);
             te[fpos[i]] = arp[i];
         }
     }
@@ -1118,7 +1119,7 @@ __device__ __forceinline__ TileDesc tile_prologue(TileSmem& S, int64_t k, const 
             sp[c] = espan[T.e0 + q];
             av[c] = aval[T.e0 + q];
         }
-        sum += static_cast<int>((sp[c] >> tile::SP_LEN) & 1023u);
+        sum += static_cast<int>((sp[c] >> tile::SP_LEN) & 1023u);  // 10-bit length
     }
     TPROF(15)
     int ptile;
@@ -1129,7 +1130,7 @@ __device__ __forceinline__ TileDesc tile_prologue(TileSmem& S, int64_t k, const 
         const int q = tid * per + c;
         if (c < per && q < T.E) {
             const int len = static_cast<int>((sp[c] >> tile::SP_LEN) & 1023u);
-            const int inrow = static_cast<int>((sp[c] >> tile::SP_IN) & 1023u);
+            const int inrow = static_cast<int>((sp[c] >> tile::SP_IN) & 4095u);
             const int prow = pre - inrow, pr = static_cast<int>(sp[c] >> tile::SP_PR);
             S.ent[q] = TileEnt{static_cast<int64_t>(sp[c] & tile::SP_BS_MASK) - pre, av[c]};
             S.ebin[q] = static_cast<uint32_t>(2 * prow) | (static_cast<uint32_t>(2 * pr) << 16);
@@ -1671,6 +1672,7 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     const int cshift = cshift_for(n);
     // 1: products, entry spans, row weights, BIG-row lists
     DBuf<int64_t> prod(ctx, m), wt(ctx, m), total(ctx, 1);
+    DBuf<int8_t> kind(ctx, m);
     DBuf<uint64_t> espan(ctx, a->nnz);
     DBuf<int32_t> lists(ctx, 2 * m), counts(ctx, 2);
     int32_t* cta_list = lists.get();
@@ -1680,7 +1682,7 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     {
         KTime kt(ctx, "row_prep");
         k_row_prep<<<grid_for(ctx, 32 * m), 256, 0, ctx->stream>>>(a->rowptr, a->colind, b->rowptr, m, prod, wt,
-                                                                   espan, lists, counts);
+                                                                   kind, espan, lists, counts);
         SPG_LAUNCH_CHECK();
     }
     {
@@ -1698,7 +1700,7 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     SPG_CUDA(cudaMemcpyAsync(&products, total.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
     {
         KTime kt(ctx, "tile_setup");
-        k_tile_flags<<<grid_for(ctx, m), 256, 0, ctx->stream>>>(wpre, prod, a->rowptr, m, flag);
+        k_tile_flags<<<grid_for(ctx, m), 256, 0, ctx->stream>>>(wpre, kind, m, flag);
         SPG_LAUNCH_CHECK();
     }
     hp.mark("launch1");
@@ -1794,8 +1796,7 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     DBuf<uint64_t> status(ctx, ntiles);
     {
         KTime kt(ctx, "tile_setup");
-        k_tile_scatter<<<grid_for(ctx, m + 1), 256, 0, ctx->stream>>>(flag, fpos,
-                                                                      prod, a->rowptr, m, tr, te);
+        k_tile_scatter<<<grid_for(ctx, m + 1), 256, 0, ctx->stream>>>(flag, fpos, kind, a->rowptr, m, tr, te);
         SPG_LAUNCH_CHECK();
     }
     SPG_CUDA(cudaMemsetAsync(status.get(), 0, ntiles * sizeof(uint64_t), ctx->stream));

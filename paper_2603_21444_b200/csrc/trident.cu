@@ -211,6 +211,8 @@ spg_csr* run_rank(spg_ctx* ctx, const std::vector<RoundPlan>& plan, const spg_cs
         }
         for (auto e : {ready[r], e0[r], e1[r], e2[r], e3[r], f0[r]}) cudaEventDestroy(e);
     }
+    big_cache_release(&cctx);
+    cudaStreamSynchronize(cs);
     cudaStreamDestroy(cs);
     return acc;
 }
