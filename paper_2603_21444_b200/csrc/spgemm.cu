@@ -1201,18 +1201,21 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
         const int W = ptile;
         const int per = ((W + NT - 1) / NT) | 1;
         const int w0 = tid * per;
+        constexpr int PERMAX = ((tile::PMAX + NT - 1) / NT) | 1;
+        uint32_t wd[PERMAX];
         uint32_t s = 0;
-        for (int q = 0; q < per; ++q)
-            if (w0 + q < W) s += S.cnt[w0 + q];
+#pragma unroll
+        for (int q = 0; q < PERMAX; ++q) {
+            wd[q] = (q < per && w0 + q < W) ? S.cnt[w0 + q] : 0u;
+            s += wd[q];
+        }
         int tot;
         const int cnt_s = static_cast<int>((s & 0xffffu) + (s >> 16));
         uint32_t p2 = static_cast<uint32_t>(tile_scan(cnt_s, &tot, S.ws[1]));
-        for (int q = 0; q < per; ++q) {
-            if (w0 + q < W) {
-                const uint32_t wd = S.cnt[w0 + q];
-                S.cnt[w0 + q] = p2 * 0x10001u + (wd << 16);
-                p2 += (wd + (wd << 16)) >> 16;
-            }
+#pragma unroll
+        for (int q = 0; q < PERMAX; ++q) {
+            if (q < per && w0 + q < W) S.cnt[w0 + q] = p2 * 0x10001u + (wd[q] << 16);
+            p2 += (wd[q] + (wd[q] << 16)) >> 16;
         }
         if (tid == 0) S.cnt[W] = static_cast<uint32_t>(ptile);  // end of the last bucket
     }
@@ -1223,6 +1226,7 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
         if (j >= nj) break;
+        uint32_t lreg = 0u;  // a >= 3 bucket whose first slot is this product
         if (bk[j] >= 0) {
             const int b = bk[j];
             const uint32_t r = __funnelshift_r(S.cnt[b >> 1], S.cnt[(b >> 1) + 1], (b & 1) << 4);
@@ -1239,9 +1243,17 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
                     aux[j] = pos | (slot << 16);
                 } else {
                     S.val[pos] = val[j];
-                    if (slot == 0) S.list[atomicAdd(&S.nlist, 1)] = r;
+                    if (slot == 0) lreg = r;  // this thread sorts the bucket
                 }
             }
+        }
+        // append >= 3 buckets to the list: one smem atomic per warp
+        const unsigned has = __ballot_sync(0xffffffffu, lreg != 0u);
+        if (has) {
+            int b0 = 0;
+            if (lane == 0) b0 = atomicAdd(&S.nlist, __popc(has));
+            b0 = __shfl_sync(0xffffffffu, b0, 0);
+            if (lreg) S.list[b0 + __popc(has & ((1u << lane) - 1u))] = lreg;
         }
     }
     TPROF(11)
@@ -1350,12 +1362,12 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
 // predecessors per round trip). Tile k only waits on tiles with smaller
 // tickets, whose CTAs publish their aggregates without waiting on anything,
 // so the chain always makes progress.
-__device__ __forceinline__ int64_t tile_look_back(TileSmem& S, uint64_t* status, int64_t k) {
+__device__ __forceinline__ int64_t tile_look_back(TileSmem& S, uint64_t* status, int64_t k, uint64_t s_first) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int64_t excl = 0;
     for (int64_t j0 = k - 1; j0 >= 0; j0 -= tile::NT) {
         const int64_t idx = j0 - tid;
-        uint64_t s = idx >= 0 ? ld_status(status + idx) : ST_INC;
+        uint64_t s = j0 == k - 1 ? s_first : (idx >= 0 ? ld_status(status + idx) : ST_INC);
         unsigned inc, upto;
         while (true) {
             inc = __ballot_sync(0xffffffffu, (s >> 62) == 2);
@@ -1432,7 +1444,8 @@ __global__ void __launch_bounds__(tile::NT, SPG_TILE_MINB) k_tile(
             TPROF(4)
         }
         // finish F: offset, row pointers, copy-out
-        const int64_t base = tile_look_back(S, status, F.k);
+        const int64_t lbi = F.k - 1 - tid;
+        const int64_t base = tile_look_back(S, status, F.k, lbi >= 0 ? ld_status(status + lbi) : ST_INC);
         TPROF(5)
         if (tid == 0 && F.k > 0) st_status(status + F.k, ST_INC | static_cast<uint64_t>(base + agg));
         if (F.big) {

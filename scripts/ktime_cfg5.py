@@ -1,0 +1,25 @@
+"""Per-kernel times of config 5 (k-mer A*A^T) (dev tool)."""
+import sys
+import time
+sys.path.insert(0, ".")
+import paper_2603_21444_b200 as spg  # noqa: E402
+
+a = spg.gen_erdos_renyi_rect(1 << 22, 1 << 18, 2.0 ** -16, 5)
+at = spg.transpose(a)
+dev = spg.Device(0)
+da, db = dev.upload(a), dev.upload(at)
+dev.timing(True)
+for _ in range(2):
+    c = dev.spgemm(da, db)
+    del c
+dev.synchronize()
+dev.timing_reset()
+t0 = time.perf_counter()
+for _ in range(3):
+    c = dev.spgemm(da, db)
+    nnz = c.nnz
+    del c
+dev.synchronize()
+print(f"config5 wall/step {1e3 * (time.perf_counter() - t0) / 3:.2f} ms nnz {nnz}")
+for k, (n, ms) in sorted(dev.timing_read().items()):
+    print(f"   {k:20s} {ms / max(n, 1):10.3f} ms x{n}")
