@@ -291,7 +291,7 @@ spg_csr* new_csr(spg_ctx* ctx, int64_t nrows, int64_t ncols, int64_t nnz) {
 
 namespace {
 constexpr size_t BIG_ROUND = size_t(64) << 20;
-constexpr size_t BIG_KEEP = 16;  // cached blocks per context
+constexpr size_t BIG_KEEP = 48;  // cached blocks per context
 }  // namespace
 
 // Best-fit block of at least `bytes` (at most 2x larger) from the context's
@@ -310,7 +310,15 @@ void* big_alloc(spg_ctx* ctx, size_t bytes, size_t* cap) {
         ctx->big_cache.erase(ctx->big_cache.begin() + best);
         return p;
     }
-    const size_t sz = (bytes + BIG_ROUND - 1) / BIG_ROUND * BIG_ROUND;
+    // fresh block: round up to a size class (64 MB steps up to 1 GB, then
+    // steps of 1/8 of the power of two) so later requests of similar size reuse it
+    size_t sz = (bytes + BIG_ROUND - 1) / BIG_ROUND * BIG_ROUND;
+    if (sz > (size_t(1) << 30)) {
+        size_t p2 = size_t(1) << 30;
+        while (p2 * 2 <= sz) p2 *= 2;
+        const size_t step = p2 / 8;
+        sz = (sz + step - 1) / step * step;
+    }
     void* p = nullptr;
     SPG_CUDA(cudaMallocFromPoolAsync(&p, sz, ctx->pool, ctx->stream));
     *cap = sz;

@@ -22,10 +22,13 @@
 // with smem atomics), each bucket is sorted by (col, x), duplicates are
 // combined in x order, and the compacted row is written to C. Bucket order is
 // row-major then column order, so the tile's output is one contiguous run of C.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <chrono>
+#include <memory>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -964,6 +967,99 @@ __global__ void k_side_scatter(const int32_t* __restrict__ rows, int n, const in
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) side_off[rows[t]] = off[t];
 }
 
+// ------------------------------------------------- BIG rows: sort-based ESC
+// Rows too large for a tile (R-MAT hubs: up to millions of products, heavy
+// duplication) are multiplied in memory-bounded batches: expand every product
+// as (row-in-batch << colbits | column, av*bv) in product order, stable radix
+// sort by that key (CUB), then sum each run of equal keys sequentially — the
+// stable sort keeps a run in product order = ascending k, so the sums are
+// bit-identical to the reference's acc[j] += av*bv.
+
+// CTA per big row: entries in chunks of NT (block scan of lengths), then the
+// warps copy the chunk's B rows (lanes over a row) to their product slots.
+__global__ void __launch_bounds__(256) k_big_expand(const int32_t* __restrict__ rows, int nrows,
+                                                    const int64_t* __restrict__ off, const int64_t* __restrict__ arp,
+                                                    const int32_t* __restrict__ acol, const double* __restrict__ aval,
+                                                    const int64_t* __restrict__ brp, const int32_t* __restrict__ bcol,
+                                                    const double* __restrict__ bval, int colbits,
+                                                    uint64_t* __restrict__ keys, double* __restrict__ vals) {
+    __shared__ int64_t s_bs[256], s_pre[257];
+    __shared__ double s_av[256];
+    __shared__ int32_t ws[9];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int r = blockIdx.x; r < nrows; r += gridDim.x) {
+        const int64_t i = rows[r];
+        const int64_t ea = arp[i], eb = arp[i + 1];
+        int64_t base = off[r];
+        const uint64_t rk = static_cast<uint64_t>(r) << colbits;
+        for (int64_t c = ea; c < eb; c += 256) {
+            const int64_t e = c + tid;
+            int len = 0;
+            if (e < eb) {
+                const int32_t k = acol[e];
+                s_bs[tid] = brp[k];
+                len = static_cast<int>(brp[k + 1] - s_bs[tid]);
+                s_av[tid] = aval[e];
+            }
+            int total;
+            const int pre = block_exclusive_scan<256>(len, &total, ws);
+            s_pre[tid] = pre;
+            if (tid == 0) s_pre[256] = total;
+            __syncthreads();
+            const int n = static_cast<int>(min(int64_t(256), eb - c));
+            for (int q = warp; q < n; q += 8) {
+                const int64_t bs = s_bs[q];
+                const int l = static_cast<int>(s_pre[q + 1] - s_pre[q]);
+                const double av = s_av[q];
+                const int64_t o = base + s_pre[q];
+                for (int x = lane; x < l; x += 32) {
+                    keys[o + x] = rk | static_cast<uint32_t>(bcol[bs + x]);
+                    vals[o + x] = dmul(av, bval[bs + x]);
+                }
+            }
+            base += total;
+            __syncthreads();
+        }
+    }
+}
+
+// flag[i] = 1 at the first element of each run of equal keys.
+__global__ void k_big_heads(const uint64_t* __restrict__ keys, int64_t n, int64_t* __restrict__ flag) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        flag[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+}
+
+// One thread per run head: the run's sum in product order.
+__global__ void k_big_runs(const uint64_t* __restrict__ keys, const double* __restrict__ vals, int64_t n,
+                           const int64_t* __restrict__ pos, int colbits, int32_t* __restrict__ ocol,
+                           double* __restrict__ oval) {
+    const uint64_t cmask = (uint64_t(1) << colbits) - 1;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const uint64_t k = keys[i];
+        if (i > 0 && keys[i - 1] == k) continue;
+        double s = dadd(0.0, vals[i]);
+        for (int64_t u = i + 1; u < n && keys[u] == k; ++u) s = dadd(s, vals[u]);
+        const int64_t o = pos[i];
+        ocol[o] = static_cast<int32_t>(k & cmask);
+        oval[o] = s;
+    }
+}
+
+// Per big row of the batch: its sorted products are [off[r], off[r+1]) of the
+// batch (keys start with the row), so its output is [pos[off[r]], pos[off[r+1]]).
+__global__ void k_big_finish(const int32_t* __restrict__ rows, int nrows, const int64_t* __restrict__ off,
+                             const int64_t* __restrict__ pos, const int32_t* ocol, const double* oval,
+                             uint64_t* __restrict__ side_cp, uint64_t* __restrict__ side_vp,
+                             int64_t* __restrict__ side_nnz) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+        const int64_t i = rows[r];
+        const int64_t f = pos[off[r]], l = pos[off[r + 1]];
+        side_cp[i] = reinterpret_cast<uint64_t>(ocol + f);
+        side_vp[i] = reinterpret_cast<uint64_t>(oval + f);
+        side_nnz[i] = l - f;
+    }
+}
+
 // Decoupled look-back status word: bits 62-63 flag (0 none, 1 aggregate,
 // 2 inclusive prefix), bits 0-61 value.
 constexpr uint64_t ST_AGG = 1ull << 62, ST_INC = 2ull << 62, ST_VAL = (1ull << 62) - 1;
@@ -1407,8 +1503,8 @@ __global__ void __launch_bounds__(tile::NT, SPG_TILE_MINB) k_tile(
     const int64_t* __restrict__ arp, const double* __restrict__ aval, const uint64_t* __restrict__ espan,
     const int32_t* __restrict__ bcol, const double* __restrict__ bval, const int64_t* __restrict__ tr,
     const int64_t* __restrict__ te, int64_t ntiles, unsigned long long* __restrict__ ticket, int cshift,
-    const int64_t* __restrict__ side_off, const int64_t* __restrict__ side_nnz,
-    const int32_t* __restrict__ side_col, const double* __restrict__ side_val, uint64_t* __restrict__ status,
+    const uint64_t* __restrict__ side_cp, const uint64_t* __restrict__ side_vp, const int64_t* __restrict__ side_nnz,
+    uint64_t* __restrict__ status,
     int64_t* __restrict__ crp, int32_t* __restrict__ ccol, double* __restrict__ cval) {
     constexpr int NT = tile::NT, NJ = tile::NJ;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1448,12 +1544,29 @@ __global__ void __launch_bounds__(tile::NT, SPG_TILE_MINB) k_tile(
         const int64_t base = tile_look_back(S, status, F.k, lbi >= 0 ? ld_status(status + lbi) : ST_INC);
         TPROF(5)
         if (tid == 0 && F.k > 0) st_status(status + F.k, ST_INC | static_cast<uint64_t>(base + agg));
-        if (F.big) {
-            const int64_t so = side_off[F.r0];
+        if (F.big) {  // copy the row's sorted product from its batch output
+            const int32_t* __restrict__ sc = reinterpret_cast<const int32_t*>(side_cp[F.r0]);
+            const double* __restrict__ sv = reinterpret_cast<const double*>(side_vp[F.r0]);
             if (tid == 0) crp[F.r0 + 1] = base + agg;
-            for (int64_t q = tid; q < agg; q += NT) {
-                ccol[base + q] = side_col[so + q];
-                cval[base + q] = side_val[so + q];
+            for (int64_t q0 = 0; q0 < agg; q0 += 4 * NT) {
+                int32_t c4[4];
+                double v4[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t q = q0 + u * NT + tid;
+                    if (q < agg) {
+                        c4[u] = sc[q];
+                        v4[u] = sv[q];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t q = q0 + u * NT + tid;
+                    if (q < agg) {
+                        ccol[base + q] = c4[u];
+                        cval[base + q] = v4[u];
+                    }
+                }
             }
         } else {
             for (int t = tid; t < F.R; t += NT) crp[F.r0 + t + 1] = base + S.rend[t];
@@ -1680,7 +1793,7 @@ struct HostProf {
 
 // Single-pass tiled multiply (the default).
 spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
-    HostProf hp;
+    HostProf hprof;
     const int64_t m = a->nrows, n = b->ncols;
     const int cshift = cshift_for(n);
     // 1: products, entry spans, row weights, BIG-row lists
@@ -1691,7 +1804,7 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     int32_t* cta_list = lists.get();
     int32_t* heavy_list = lists.get() + m;
     SPG_CUDA(cudaMemsetAsync(counts.get(), 0, 2 * sizeof(int32_t), ctx->stream));
-    hp.mark("alloc1");
+    hprof.mark("alloc1");
     {
         KTime kt(ctx, "row_prep");
         k_row_prep<<<grid_for(ctx, 32 * m), 256, 0, ctx->stream>>>(a->rowptr, a->colind, b->rowptr, m, prod, wt,
@@ -1716,44 +1829,20 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
         k_tile_flags<<<grid_for(ctx, m), 256, 0, ctx->stream>>>(wpre, kind, m, flag);
         SPG_LAUNCH_CHECK();
     }
-    hp.mark("launch1");
+    hprof.mark("launch1");
     SPG_CUDA(cudaStreamSynchronize(ctx->stream));
-    hp.mark("sync1");
+    hprof.mark("sync1");
     const int ncta = hc[0], nheavy = hc[1], nside = ncta + nheavy;
 
-    // 3: BIG rows into a side buffer (symbolic, offsets, numeric)
-    DBuf<int64_t> rnnz(ctx, m), side_off(ctx, m);
-    std::vector<int64_t> hp_off(nheavy + 1, 0), he_off(nheavy + 1, 0), hb_off(nheavy + 1, 0);
-    if (nheavy) {
-        DBuf<int64_t> info(ctx, 2 * int64_t(nheavy));
-        k_heavy_info<<<grid_for(ctx, nheavy), 256, 0, ctx->stream>>>(heavy_list, nheavy, prod, a->rowptr, info);
-        SPG_LAUNCH_CHECK();
-        std::vector<int64_t> hinfo(2 * size_t(nheavy));
-        SPG_CUDA(cudaMemcpyAsync(hinfo.data(), info.get(), hinfo.size() * sizeof(int64_t), cudaMemcpyDeviceToHost,
-                                 ctx->stream));
-        SPG_CUDA(cudaStreamSynchronize(ctx->stream));
-        for (int h = 0; h < nheavy; ++h) {
-            hp_off[h + 1] = hp_off[h] + hinfo[2 * h];
-            he_off[h + 1] = he_off[h] + hinfo[2 * h + 1] + 1;
-            hb_off[h + 1] = hb_off[h] + (hinfo[2 * h] + BUCKET_LOAD - 1) / BUCKET_LOAD + 1;
-        }
-    }
-    DBuf<int64_t> d_hp(ctx, nheavy + 1), d_he(ctx, nheavy + 1), d_hb(ctx, nheavy + 1);
-    DBuf<int64_t> w_epre(ctx, he_off[nheavy]);
-    DBuf<int32_t> w_col(ctx, hp_off[nheavy]), w_bkt(ctx, hp_off[nheavy]), w_perm(ctx, hp_off[nheavy]);
-    DBuf<double> w_val(ctx, hp_off[nheavy]);
-    DBuf<int64_t> w_boff(ctx, hb_off[nheavy]), w_bcnt(ctx, hb_off[nheavy]);
-    HeavyWs hws{};
-    if (nheavy) {
-        SPG_CUDA(cudaMemcpyAsync(d_hp.get(), hp_off.data(), (nheavy + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
-        SPG_CUDA(cudaMemcpyAsync(d_he.get(), he_off.data(), (nheavy + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
-        SPG_CUDA(cudaMemcpyAsync(d_hb.get(), hb_off.data(), (nheavy + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
-        hws = HeavyWs{w_epre, w_col, w_val, w_bkt, w_perm, w_boff, w_bcnt};
-    }
-    const size_t cta_smem = sizeof(CtaSmem);
+    // 3: BIG rows: sort-based ESC in batches bounded by products
+    const int nbig = ncta + nheavy;
+    DBuf<uint64_t> side_cp(ctx, nbig ? m : 1), side_vp(ctx, nbig ? m : 1);
+    DBuf<int64_t> side_nnz(ctx, nbig ? m : 1);
+    std::vector<std::unique_ptr<DBuf<int32_t>>> outc;
+    std::vector<std::unique_ptr<DBuf<double>>> outv;
     if (!ctx->tile_attr_set) {
-        SPG_CUDA(cudaFuncSetAttribute(k_cta_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cta_smem));
-        SPG_CUDA(cudaFuncSetAttribute(k_cta_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cta_smem));
+        SPG_CUDA(cudaFuncSetAttribute(k_cta_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CtaSmem)));
+        SPG_CUDA(cudaFuncSetAttribute(k_cta_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CtaSmem)));
         SPG_CUDA(cudaFuncSetAttribute(k_warp_numeric<WPB, 8, NUM8_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(sizeof(WarpRowSmem<8>) * WPB)));
         SPG_CUDA(cudaFuncSetAttribute(k_warp_numeric<WPB, 16, NUM16_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1761,50 +1850,101 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
         SPG_CUDA(cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem)));
         ctx->tile_attr_set = true;
     }
-    int64_t side_total = 0;
-    DBuf<int64_t> sn(ctx, nside + 1), so(ctx, nside + 1);
-    if (nside) {
-        KTime kt(ctx, "side_rows");
-        const int gc = std::max(1, std::min(ncta, ctx->num_sms * 2));
-        if (ncta)
-            k_cta_rows<false><<<gc, NT, cta_smem, ctx->stream>>>(a->rowptr, a->colind, a->values, b->rowptr,
-                                                                 b->colind, b->values, prod, cta_list, counts.get(),
-                                                                 rnnz, nullptr, nullptr, nullptr);
-        if (nheavy)
-            k_heavy<false><<<nheavy, NT, 0, ctx->stream>>>(a->rowptr, a->colind, a->values, b->rowptr, b->colind,
-                                                           b->values, heavy_list, d_hp, d_he, d_hb, hws, rnnz, nullptr,
-                                                           nullptr, nullptr);
+    if (nbig) {
+        KTime kt(ctx, "big_rows");
+        // the big rows (both lists), ascending, and their products
+        std::vector<int32_t> hrows(nbig);
+        SPG_CUDA(cudaMemcpyAsync(hrows.data(), cta_list, ncta * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+        SPG_CUDA(cudaMemcpyAsync(hrows.data() + ncta, heavy_list, nheavy * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+        SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+        std::sort(hrows.begin(), hrows.end());
+        DBuf<int32_t> drows(ctx, nbig);
+        DBuf<int64_t> dprod(ctx, nbig);
+        SPG_CUDA(cudaMemcpyAsync(drows.get(), hrows.data(), nbig * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+        k_side_gather<<<grid_for(ctx, nbig), 256, 0, ctx->stream>>>(drows, nbig, prod, dprod);
         SPG_LAUNCH_CHECK();
-        if (ncta) k_side_gather<<<grid_for(ctx, ncta), 256, 0, ctx->stream>>>(cta_list, ncta, rnnz, sn);
-        if (nheavy) k_side_gather<<<grid_for(ctx, nheavy), 256, 0, ctx->stream>>>(heavy_list, nheavy, rnnz, sn.get() + ncta);
-        SPG_LAUNCH_CHECK();
-        exclusive_scan_i64(ctx, sn, so, nside);
-        if (ncta) k_side_scatter<<<grid_for(ctx, ncta), 256, 0, ctx->stream>>>(cta_list, ncta, so, side_off);
-        if (nheavy)
-            k_side_scatter<<<grid_for(ctx, nheavy), 256, 0, ctx->stream>>>(heavy_list, nheavy, so.get() + ncta, side_off);
-        SPG_LAUNCH_CHECK();
-        side_total = read_scalar(ctx, so.get() + nside);
+        std::vector<int64_t> hp(nbig);
+        SPG_CUDA(cudaMemcpyAsync(hp.data(), dprod.get(), nbig * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+        int colbits = 1;
+        while ((int64_t(1) << colbits) < n) ++colbits;
+        int64_t bmax = int64_t(300) << 20;  // products per batch (~48 B of workspace each)
+        for (int64_t v : hp) bmax = std::max(bmax, v);
+        std::vector<int> cut{0};  // batches of consecutive big rows
+        for (int64_t r = 0, acc = 0; r < nbig; ++r) {
+            if (r > cut.back() && acc + hp[r] > bmax) {
+                cut.push_back(static_cast<int>(r));
+                acc = 0;
+            }
+            acc += hp[r];
+        }
+        cut.push_back(nbig);
+        int64_t pmax = 0;
+        for (size_t t = 0; t + 1 < cut.size(); ++t) {
+            int64_t P = 0;
+            for (int r = cut[t]; r < cut[t + 1]; ++r) P += hp[r];
+            pmax = std::max(pmax, P);
+        }
+        DBuf<uint64_t> keys(ctx, pmax), keys2(ctx, pmax);
+        DBuf<double> vals(ctx, pmax), vals2(ctx, pmax);
+        DBuf<int64_t> flagb(ctx, pmax), posb(ctx, pmax + 1), doff(ctx, nbig + 1);
+        size_t tmp_bytes = 0;
+        SPG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.get(), keys2.get(), vals.get(), vals2.get(),
+                                                 std::max<int64_t>(pmax, 1), 0, 64, ctx->stream));
+        DBuf<unsigned char> tmp(ctx, tmp_bytes);
+        std::vector<int64_t> hoff(nbig + 1);
+        for (size_t t = 0; t + 1 < cut.size(); ++t) {
+            const int r0 = cut[t], nb = cut[t + 1] - cut[t];
+            hoff[0] = 0;
+            for (int r = 0; r < nb; ++r) hoff[r + 1] = hoff[r] + hp[r0 + r];
+            const int64_t P = hoff[nb];
+            SPG_CUDA(cudaMemcpyAsync(doff.get(), hoff.data(), (nb + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
+                                     ctx->stream));
+            int rowbits = 1;
+            while ((int64_t(1) << rowbits) < nb) ++rowbits;
+            int64_t total = 0;
+            hprof.mark("big_batch_setup");
+            if (P > 0) {
+                KTime kx(ctx, "big_expand");
+                k_big_expand<<<std::min(nb, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+                    drows.get() + r0, nb, doff, a->rowptr, a->colind, a->values, b->rowptr, b->colind, b->values,
+                    colbits, keys, vals);
+                SPG_LAUNCH_CHECK();
+            }
+            if (P > 0) {
+                KTime ks(ctx, "big_sort");
+                SPG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tmp_bytes, keys.get(), keys2.get(), vals.get(),
+                                                         vals2.get(), P, 0, colbits + rowbits, ctx->stream));
+            }
+            if (P > 0) {
+                k_big_heads<<<grid_for(ctx, P), 256, 0, ctx->stream>>>(keys2, P, flagb);
+                SPG_LAUNCH_CHECK();
+                exclusive_scan_i64(ctx, flagb, posb, P);
+                total = read_scalar(ctx, posb.get() + P);
+            }
+            outc.emplace_back(new DBuf<int32_t>(ctx, total));
+            outv.emplace_back(new DBuf<double>(ctx, total));
+            hprof.mark("big_scan");
+            if (P > 0) {
+                KTime kr(ctx, "big_runs");
+                k_big_runs<<<grid_for(ctx, P), 256, 0, ctx->stream>>>(keys2, vals2, P, posb, colbits,
+                                                                       outc.back()->get(), outv.back()->get());
+                SPG_LAUNCH_CHECK();
+            }
+            if (P == 0) SPG_CUDA(cudaMemsetAsync(posb.get(), 0, sizeof(int64_t), ctx->stream));
+            k_big_finish<<<grid_for(ctx, nb), 256, 0, ctx->stream>>>(drows.get() + r0, nb, doff, posb,
+                                                                     outc.back()->get(), outv.back()->get(), side_cp,
+                                                                     side_vp, side_nnz);
+            SPG_LAUNCH_CHECK();
+            hprof.mark("big_runs");
+        }
     }
-    DBuf<int32_t> s_col(ctx, side_total);
-    DBuf<double> s_val(ctx, side_total);
-    if (nside) {
-        KTime kt(ctx, "side_rows");
-        const int gc = std::max(1, std::min(ncta, ctx->num_sms * 2));
-        if (ncta)
-            k_cta_rows<true><<<gc, NT, cta_smem, ctx->stream>>>(a->rowptr, a->colind, a->values, b->rowptr, b->colind,
-                                                                b->values, prod, cta_list, counts.get(), nullptr,
-                                                                side_off, s_col, s_val);
-        if (nheavy)
-            k_heavy<true><<<nheavy, NT, 0, ctx->stream>>>(a->rowptr, a->colind, a->values, b->rowptr, b->colind,
-                                                          b->values, heavy_list, d_hp, d_he, d_hb, hws, nullptr,
-                                                          side_off, s_col, s_val);
-        SPG_LAUNCH_CHECK();
-    }
-    hp.mark("side");
+    hprof.mark("side");
     // 4: tiles
     exclusive_scan_i64(ctx, flag, fpos, m);
     const int64_t ntiles = read_scalar(ctx, fpos.get() + m);
-    hp.mark("tilescan");
+    hprof.mark("tilescan");
     DBuf<int64_t> tr(ctx, ntiles + 1), te(ctx, ntiles + 1);
     DBuf<uint64_t> status(ctx, ntiles);
     {
@@ -1816,9 +1956,9 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     DBuf<unsigned long long> ticket(ctx, 1);
     SPG_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned long long), ctx->stream));
     spg_csr* c = new_csr(ctx, m, n, -1);
-    hp.mark("tilesetup");
+    hprof.mark("tilesetup");
     alloc_c_arrays(ctx, c, products);  // upper bound of nnz(C)
-    hp.mark("allocC");
+    hprof.mark("allocC");
     SPG_CUDA(cudaMemsetAsync(c->rowptr, 0, sizeof(int64_t), ctx->stream));
     int occ = 1;
     SPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile, tile::NT, sizeof(TileSmem)));
@@ -1826,13 +1966,13 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     {
         KTime kt(ctx, "spgemm_tile");
         k_tile<<<grid, tile::NT, sizeof(TileSmem), ctx->stream>>>(a->rowptr, a->values, espan, b->colind, b->values,
-                                                                  tr, te, ntiles, ticket, cshift, side_off, rnnz, s_col,
-                                                                  s_val, status, c->rowptr, c->colind, c->values);
+                                                                  tr, te, ntiles, ticket, cshift, side_cp, side_vp,
+                                                                  side_nnz, status, c->rowptr, c->colind, c->values);
         SPG_LAUNCH_CHECK();
     }
-    hp.mark("launch_tile");
+    hprof.mark("launch_tile");
     c->nnz = read_scalar(ctx, c->rowptr + m);
-    hp.mark("tile");
+    hprof.mark("tile");
     return c;
 }
 }  // namespace

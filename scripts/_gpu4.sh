@@ -1,3 +1,4 @@
 timeout 600 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -1
-python scripts/ktime.py 4194304 16 3 | head -3
-for v in w1792m3 nt128w1024 w2560; do SPG_LIB_PATH=$PWD/var/$v/libspgb200.so timeout 120 python scripts/ktime.py 4194304 16 3 | head -3; done
+python scripts/ktime_rmat.py 18 2>&1 | tail -9
+timeout 900 python scripts/configs.py --configs 1,2,4,5 > gpurun_out/configs.jsonl 2> gpurun_out/configs.err; cat gpurun_out/configs.jsonl; tail -2 gpurun_out/configs.err
+timeout 900 python scripts/configs.py --configs 3 --rmat-scale 18 >> gpurun_out/configs.jsonl 2>> gpurun_out/configs.err; tail -1 gpurun_out/configs.jsonl

@@ -19,9 +19,12 @@ dev.timing(True)
 c = dev.spgemm(da, da)
 dev.synchronize()
 dev.timing_reset()
+reps = 3
 t0 = time.perf_counter()
-c = dev.spgemm(da, da)
-dev.synchronize()
-print(f"wall {1e3 * (time.perf_counter() - t0):.1f} ms nnzC={c.nnz}")
+for _ in range(reps):
+    del c
+    c = dev.spgemm(da, da)
+    dev.synchronize()
+print(f"wall {1e3 * (time.perf_counter() - t0) / reps:.1f} ms/step nnzC={c.nnz}")
 for k, (n, ms) in sorted(dev.timing_read().items()):
-    print(f"   {k:20s} {ms / max(n, 1):10.3f} ms x{n}")
+    print(f"   {k:20s} {ms / reps:10.3f} ms/step ({n // reps} launches)")
