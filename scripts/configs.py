@@ -156,6 +156,11 @@ def main():
                 nxt = int(np.searchsorted(cum, base + args.batch_products, side="right"))
                 cuts.append(max(nxt, cuts[-1] + 1) if nxt < a.nrows else int(a.nrows))
             dev.synchronize()
+            # warm-up on the first batch (allocations, first launches)
+            ab = dev.extract(da, cuts[0], cuts[1], 0, int(a.ncols))
+            cb = dev.spgemm(ab, da)
+            del ab, cb
+            dev.synchronize()
             nnz = 0
             t1 = time.perf_counter()
             for r0, r1 in zip(cuts[:-1], cuts[1:]):
