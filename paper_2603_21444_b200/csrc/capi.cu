@@ -96,6 +96,8 @@ spg_status spg_init(int device, spg_ctx** out) {
         const char* tp = std::getenv("SPG_TWO_PASS");
         ctx->two_pass = (tp && tp[0] == '1') ? 1 : 0;
         SPG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        for (int i = 0; i < spg_ctx::NAUX; ++i) SPG_CUDA(cudaStreamCreateWithFlags(&ctx->aux[i], cudaStreamNonBlocking));
+        for (auto& e : ctx->aux_ev) SPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         SPG_CUDA(cudaDeviceGetDefaultMemPool(&ctx->pool, device));
         uint64_t keep = UINT64_MAX;  // keep freed blocks cached in the pool
         SPG_CUDA(cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &keep));
@@ -137,6 +139,8 @@ spg_status spg_finalize(spg_ctx* ctx) {
         }
         for (auto e : ctx->timer.pool) cudaEventDestroy(e);
         cudaFreeHost(ctx->host_scalars);
+        for (auto st : ctx->aux) cudaStreamDestroy(st);
+        for (auto e : ctx->aux_ev) cudaEventDestroy(e);
         cudaStreamDestroy(ctx->stream);
         delete ctx;
     });

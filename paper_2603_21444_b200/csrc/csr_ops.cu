@@ -4,6 +4,7 @@
 //   extract  (reference partition.cpp:161-222, one tile)
 //   column_normalize / prune (reference csr.cpp:224-249) — MCL post-step
 //   check_canonical (reference csr.cpp:30-50)
+#include <algorithm>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -431,6 +432,7 @@ spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n) {
     }
     spg_csr* out = new_csr(ctx, rows, ncols, nnz);
     SPG_CUDA(cudaMemsetAsync(out->rowptr, 0, sizeof(int64_t), ctx->stream));
+    if (n > 1 && ctx->aux[0]) SPG_CUDA(cudaEventRecord(ctx->aux_ev[spg_ctx::NAUX], ctx->stream));  // fork point
     int64_t r = 0, base = 0;
     const int dd = ctx->device;
     for (int s = 0; s < n; ++s) {
@@ -448,17 +450,29 @@ spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n) {
             SPG_LAUNCH_CHECK();
         }
         if (sl->nnz) {
+            // slices are pulled concurrently by the copy engines (one aux stream
+            // each, forked from and joined back into the context stream)
+            cudaStream_t st = ctx->stream;
+            if (n > 1 && ctx->aux[0]) {
+                st = ctx->aux[s % spg_ctx::NAUX];
+                if (s < spg_ctx::NAUX) SPG_CUDA(cudaStreamWaitEvent(st, ctx->aux_ev[spg_ctx::NAUX], 0));
+            }
             if (sd == dd) {
-                SPG_CUDA(cudaMemcpyAsync(out->colind + base, sl->colind, sl->nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
-                SPG_CUDA(cudaMemcpyAsync(out->values + base, sl->values, sl->nnz * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+                SPG_CUDA(cudaMemcpyAsync(out->colind + base, sl->colind, sl->nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+                SPG_CUDA(cudaMemcpyAsync(out->values + base, sl->values, sl->nnz * sizeof(double), cudaMemcpyDeviceToDevice, st));
             } else {
-                SPG_CUDA(cudaMemcpyPeerAsync(out->colind + base, dd, sl->colind, sd, sl->nnz * sizeof(int32_t), ctx->stream));
-                SPG_CUDA(cudaMemcpyPeerAsync(out->values + base, dd, sl->values, sd, sl->nnz * sizeof(double), ctx->stream));
+                SPG_CUDA(cudaMemcpyPeerAsync(out->colind + base, dd, sl->colind, sd, sl->nnz * sizeof(int32_t), st));
+                SPG_CUDA(cudaMemcpyPeerAsync(out->values + base, dd, sl->values, sd, sl->nnz * sizeof(double), st));
             }
         }
         r += sl->nrows;
         base += sl->nnz;
     }
+    if (n > 1 && ctx->aux[0])
+        for (int i = 0; i < std::min(n, spg_ctx::NAUX); ++i) {
+            SPG_CUDA(cudaEventRecord(ctx->aux_ev[i], ctx->aux[i]));
+            SPG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[i], 0));
+        }
     return out;
 }
 

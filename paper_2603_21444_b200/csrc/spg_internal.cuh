@@ -66,6 +66,10 @@ struct spg_ctx {
     // Pinned host staging for small scalar read-backs.
     int64_t* host_scalars = nullptr;
     bool tile_attr_set = false;
+    // fork/join streams for concurrent slice copies (vconcat pulls from several peers at once)
+    static constexpr int NAUX = 4;
+    cudaStream_t aux[NAUX] = {};
+    cudaEvent_t aux_ev[NAUX + 1] = {};
     // Large C arrays (>= 256 MB) come from this block cache instead of the pool:
     // the pool splits freed blocks for smaller requests, after which a
     // multi-GB request maps fresh memory on every call (see big_alloc).
