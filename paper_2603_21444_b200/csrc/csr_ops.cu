@@ -292,8 +292,25 @@ spg_csr* new_csr(spg_ctx* ctx, int64_t nrows, int64_t ncols, int64_t nnz) {
 
 namespace {
 constexpr size_t BIG_ROUND = size_t(64) << 20;
-constexpr size_t BIG_KEEP = 48;  // cached blocks per context
+constexpr size_t BIG_KEEP = 48;                        // cached blocks per context
+constexpr size_t BIG_KEEP_BYTES = size_t(32) << 30;    // and at most this many bytes
 }  // namespace
+
+void* pool_alloc(spg_ctx* ctx, size_t bytes) {
+    void* p = nullptr;
+    cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, ctx->pool, ctx->stream);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        big_cache_release(ctx);
+        cudaStreamSynchronize(ctx->stream);
+        cudaMemPoolTrimTo(ctx->pool, 0);
+        e = cudaMallocFromPoolAsync(&p, bytes, ctx->pool, ctx->stream);
+    }
+    if (e != cudaSuccess)
+        fail(e == cudaErrorMemoryAllocation ? SPG_OOM : SPG_CUDA_ERROR,
+             "device allocation of " + std::to_string(bytes) + " bytes failed: " + cudaGetErrorString(e));
+    return p;
+}
 
 // Best-fit block of at least `bytes` (at most 2x larger) from the context's
 // cache, else a fresh pool block rounded up to 64 MB. Stream order on the
@@ -320,14 +337,20 @@ void* big_alloc(spg_ctx* ctx, size_t bytes, size_t* cap) {
         const size_t step = p2 / 8;
         sz = (sz + step - 1) / step * step;
     }
-    void* p = nullptr;
-    SPG_CUDA(cudaMallocFromPoolAsync(&p, sz, ctx->pool, ctx->stream));
+    void* p = pool_alloc(ctx, sz);
     *cap = sz;
     return p;
 }
 
 void big_free(spg_ctx* ctx, void* p, size_t cap) {
     ctx->big_cache.emplace_back(p, cap);
+    size_t held = 0;
+    for (auto& b : ctx->big_cache) held += b.second;
+    while (held > BIG_KEEP_BYTES && ctx->big_cache.size() > 1) {  // drop the oldest
+        held -= ctx->big_cache.front().second;
+        cudaFreeAsync(ctx->big_cache.front().first, ctx->stream);
+        ctx->big_cache.erase(ctx->big_cache.begin());
+    }
     if (ctx->big_cache.size() > BIG_KEEP) {  // drop the smallest
         size_t k = 0;
         for (size_t i = 1; i < ctx->big_cache.size(); ++i)

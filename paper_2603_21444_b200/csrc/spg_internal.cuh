@@ -103,12 +103,14 @@ struct DeviceScope {
     }
 };
 
+// Stream-ordered pool allocation; on OOM the context's block cache and the
+// pool's cached memory are released and the allocation retried once.
+void* pool_alloc(spg_ctx* ctx, size_t bytes);
+
 template <class T>
 T* dalloc(spg_ctx* ctx, size_t n) {
-    void* p = nullptr;
     if (n == 0) n = 1;
-    SPG_CUDA(cudaMallocFromPoolAsync(&p, n * sizeof(T), ctx->pool, ctx->stream));
-    return static_cast<T*>(p);
+    return static_cast<T*>(pool_alloc(ctx, n * sizeof(T)));
 }
 
 inline void dfree(spg_ctx* ctx, void* p) {
