@@ -1,5 +1,6 @@
 // C-ABI entry points of libspgb200.so (include/spg/capi.h). Every function
 // catches, records the message in a thread-local buffer and returns a status.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -53,6 +54,27 @@ void flush_timer(spg_ctx* ctx) {
     t.pending.clear();
 }
 }  // namespace
+
+// Host <-> device copy in 64 MB chunks spread over the context's copy streams
+// (several DMA transfers in flight use the PCIe link better than one), forked
+// from and joined back into the context stream.
+void copy_chunked(spg_ctx* ctx, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+    constexpr size_t CH = size_t(64) << 20;
+    if (bytes < 2 * CH || !ctx->aux[0]) {
+        SPG_CUDA(cudaMemcpyAsync(dst, src, bytes, kind, ctx->stream));
+        return;
+    }
+    SPG_CUDA(cudaEventRecord(ctx->aux_ev[spg_ctx::NAUX], ctx->stream));
+    for (int i = 0; i < spg_ctx::NAUX; ++i) SPG_CUDA(cudaStreamWaitEvent(ctx->aux[i], ctx->aux_ev[spg_ctx::NAUX], 0));
+    int c = 0;
+    for (size_t off = 0; off < bytes; off += CH, ++c)
+        SPG_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off,
+                                 std::min(CH, bytes - off), kind, ctx->aux[c % spg_ctx::NAUX]));
+    for (int i = 0; i < spg_ctx::NAUX; ++i) {
+        SPG_CUDA(cudaEventRecord(ctx->aux_ev[i], ctx->aux[i]));
+        SPG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[i], 0));
+    }
+}
 
 extern "C" {
 
@@ -216,7 +238,7 @@ spg_status spg_csr_upload(spg_ctx* ctx, int64_t nrows, int64_t ncols, const int6
         SPG_CUDA(cudaMemcpyAsync(m->rowptr, rowptr, (nrows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
         if (nnz) {
             if (colind_width == 4) {
-                SPG_CUDA(cudaMemcpyAsync(m->colind, colind, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+                copy_chunked(ctx, m->colind, colind, nnz * sizeof(int32_t), cudaMemcpyHostToDevice);
             } else {
                 DBuf<int64_t> wide(ctx, nnz);
                 SPG_CUDA(cudaMemcpyAsync(wide.get(), colind, nnz * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
@@ -227,7 +249,7 @@ spg_status spg_csr_upload(spg_ctx* ctx, int64_t nrows, int64_t ncols, const int6
                     throw;
                 }
             }
-            SPG_CUDA(cudaMemcpyAsync(m->values, values, nnz * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+            copy_chunked(ctx, m->values, values, nnz * sizeof(double), cudaMemcpyHostToDevice);
         }
         *out = m;
     });
@@ -262,8 +284,8 @@ spg_status spg_csr_upload_into(spg_ctx* ctx, spg_csr* m, const int64_t* rowptr, 
         cudaStream_t st = m->ctx->stream;
         SPG_CUDA(cudaMemcpyAsync(m->rowptr, rowptr, (m->nrows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
         if (m->nnz) {
-            SPG_CUDA(cudaMemcpyAsync(m->colind, colind, m->nnz * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-            SPG_CUDA(cudaMemcpyAsync(m->values, values, m->nnz * sizeof(double), cudaMemcpyHostToDevice, st));
+            copy_chunked(m->ctx, m->colind, colind, m->nnz * sizeof(int32_t), cudaMemcpyHostToDevice);
+            copy_chunked(m->ctx, m->values, values, m->nnz * sizeof(double), cudaMemcpyHostToDevice);
         }
         SPG_CUDA(cudaStreamSynchronize(st));
     });
@@ -285,8 +307,7 @@ spg_status spg_csr_download(spg_ctx* ctx, const spg_csr* m, int64_t* rowptr, voi
                                      ctx->stream));
         if (colind && src->nnz) {
             if (colind_width == 4) {
-                SPG_CUDA(cudaMemcpyAsync(colind, src->colind, src->nnz * sizeof(int32_t), cudaMemcpyDeviceToHost,
-                                         ctx->stream));
+                copy_chunked(ctx, colind, src->colind, src->nnz * sizeof(int32_t), cudaMemcpyDeviceToHost);
             } else {
                 DBuf<int64_t> wide(ctx, src->nnz);
                 widen_index(ctx, src->colind, wide, src->nnz);
@@ -294,8 +315,7 @@ spg_status spg_csr_download(spg_ctx* ctx, const spg_csr* m, int64_t* rowptr, voi
                                          ctx->stream));
             }
         }
-        if (values && src->nnz)
-            SPG_CUDA(cudaMemcpyAsync(values, src->values, src->nnz * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        if (values && src->nnz) copy_chunked(ctx, values, src->values, src->nnz * sizeof(double), cudaMemcpyDeviceToHost);
         SPG_CUDA(cudaStreamSynchronize(ctx->stream));
         if (tmp) free_csr(tmp);
     });
