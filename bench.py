@@ -338,6 +338,12 @@ def ours_multi(args):
     import torch
     import torch.distributed as dist
 
+    # NCCL's init banner (and any other C-level stdout) goes to stderr; the one
+    # JSON line is written to the original stdout
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
+
     import paper_2603_21444_b200 as spg
     from paper_2603_21444_b200 import dist as sd
 
@@ -485,7 +491,8 @@ def ours_multi(args):
             "clocks": clk.summary(),
             "gpu_launches": int(lt.item()),
         }
-        print(json.dumps(line), flush=True)
+        sys.stdout.flush()
+        os.write(json_fd, (json.dumps(line) + "\n").encode())
     ex.close()
     dist.barrier()
     dist.destroy_process_group()

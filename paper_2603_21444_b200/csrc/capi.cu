@@ -119,6 +119,7 @@ spg_status spg_init(int device, spg_ctx** out) {
         ctx->two_pass = (tp && tp[0] == '1') ? 1 : 0;
         SPG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         for (int i = 0; i < spg_ctx::NAUX; ++i) SPG_CUDA(cudaStreamCreateWithFlags(&ctx->aux[i], cudaStreamNonBlocking));
+        SPG_CUDA(cudaStreamCreateWithFlags(&ctx->xfer, cudaStreamNonBlocking));
         for (auto& e : ctx->aux_ev) SPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         SPG_CUDA(cudaDeviceGetDefaultMemPool(&ctx->pool, device));
         uint64_t keep = UINT64_MAX;  // keep freed blocks cached in the pool
@@ -162,6 +163,7 @@ spg_status spg_finalize(spg_ctx* ctx) {
         for (auto e : ctx->timer.pool) cudaEventDestroy(e);
         cudaFreeHost(ctx->host_scalars);
         for (auto st : ctx->aux) cudaStreamDestroy(st);
+        cudaStreamDestroy(ctx->xfer);
         for (auto e : ctx->aux_ev) cudaEventDestroy(e);
         cudaStreamDestroy(ctx->stream);
         delete ctx;

@@ -69,6 +69,7 @@ struct spg_ctx {
     // fork/join streams for concurrent slice copies (vconcat pulls from several peers at once)
     static constexpr int NAUX = 4;
     cudaStream_t aux[NAUX] = {};
+    cudaStream_t xfer = nullptr;  // trident rounds: tile pulls of the next round
     cudaEvent_t aux_ev[NAUX + 1] = {};
     // Large C arrays (>= 256 MB) come from this block cache instead of the pool:
     // the pool splits freed blocks for smaller requests, after which a

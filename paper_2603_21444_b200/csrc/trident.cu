@@ -137,8 +137,7 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 spg_csr* run_rank(spg_ctx* ctx, const std::vector<RoundPlan>& plan, const spg_csr* const* a_views,
                   const spg_csr* const* b_views, int64_t c_rows, int64_t c_cols, double* tl /* rounds*4 */) {
     DeviceScope ds(ctx->device);
-    cudaStream_t cs;
-    SPG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaStream_t cs = ctx->xfer;  // persistent transfer stream of the context
     spg_ctx cctx = *ctx;  // same device and pool, copy stream
     cctx.stream = cs;
     cctx.big_cache.clear();  // the block cache belongs to ctx (its stream orders reuse)
@@ -147,8 +146,8 @@ spg_csr* run_rank(spg_ctx* ctx, const std::vector<RoundPlan>& plan, const spg_cs
     std::vector<spg_csr*> a_in(R, nullptr), b_in(R, nullptr);
     std::vector<bool> a_owned(R, false), b_owned(R, false);
     std::vector<cudaEvent_t> ready(R), e0(R), e1(R), e2(R), e3(R), f0(R);
-    for (int r = 0; r < R; ++r) {
-        for (auto* e : {&ready[r], &e0[r], &e1[r], &e2[r], &e3[r], &f0[r]}) SPG_CUDA(cudaEventCreate(e));
+    for (int r = 0; r < R; ++r) {  // events from the context's pool (returned below)
+        for (auto* e : {&ready[r], &e0[r], &e1[r], &e2[r], &e3[r], &f0[r]}) *e = ctx->timer.ev();
     }
     auto issue_fetch = [&](int r) {
         SPG_CUDA(cudaEventRecord(f0[r], cs));
@@ -209,11 +208,10 @@ spg_csr* run_rank(spg_ctx* ctx, const std::vector<RoundPlan>& plan, const spg_cs
             tl[r * 4 + 2] = elapsed(e1[r], e2[r]);     // local multiply
             tl[r * 4 + 3] = elapsed(e2[r], e3[r]);     // partial-C merge
         }
-        for (auto e : {ready[r], e0[r], e1[r], e2[r], e3[r], f0[r]}) cudaEventDestroy(e);
+        for (auto e : {ready[r], e0[r], e1[r], e2[r], e3[r], f0[r]}) ctx->timer.pool.push_back(e);
     }
     big_cache_release(&cctx);
     cudaStreamSynchronize(cs);
-    cudaStreamDestroy(cs);
     return acc;
 }
 
