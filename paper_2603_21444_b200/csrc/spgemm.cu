@@ -1060,6 +1060,41 @@ __global__ void k_big_finish(const int32_t* __restrict__ rows, int nrows, const 
     }
 }
 
+// BIG rows' sorted products into C[crp[r], crp[r+1]) (after k_tile wrote the
+// row pointers): one CTA-range per row chunk, 16 independent copies per thread
+// in flight.
+__global__ void __launch_bounds__(256) k_big_copy(const int32_t* __restrict__ rows, int nrows,
+                                                  const uint64_t* __restrict__ side_cp,
+                                                  const uint64_t* __restrict__ side_vp, const int64_t* __restrict__ crp,
+                                                  int32_t* __restrict__ ccol, double* __restrict__ cval) {
+    for (int r = blockIdx.x; r < nrows; r += gridDim.x) {
+        const int64_t i = rows[r];
+        const int64_t base = crp[i], n = crp[i + 1] - base;
+        const int32_t* __restrict__ sc = reinterpret_cast<const int32_t*>(side_cp[i]);
+        const double* __restrict__ sv = reinterpret_cast<const double*>(side_vp[i]);
+        for (int64_t q0 = 0; q0 < n; q0 += 8 * 256) {
+            int32_t c8[8];
+            double v8[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t q = q0 + u * 256 + threadIdx.x;
+                if (q < n) {
+                    c8[u] = sc[q];
+                    v8[u] = sv[q];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t q = q0 + u * 256 + threadIdx.x;
+                if (q < n) {
+                    ccol[base + q] = c8[u];
+                    cval[base + q] = v8[u];
+                }
+            }
+        }
+    }
+}
+
 // Decoupled look-back status word: bits 62-63 flag (0 none, 1 aggregate,
 // 2 inclusive prefix), bits 0-61 value.
 constexpr uint64_t ST_AGG = 1ull << 62, ST_INC = 2ull << 62, ST_VAL = (1ull << 62) - 1;
@@ -1544,30 +1579,8 @@ __global__ void __launch_bounds__(tile::NT, SPG_TILE_MINB) k_tile(
         const int64_t base = tile_look_back(S, status, F.k, lbi >= 0 ? ld_status(status + lbi) : ST_INC);
         TPROF(5)
         if (tid == 0 && F.k > 0) st_status(status + F.k, ST_INC | static_cast<uint64_t>(base + agg));
-        if (F.big) {  // copy the row's sorted product from its batch output
-            const int32_t* __restrict__ sc = reinterpret_cast<const int32_t*>(side_cp[F.r0]);
-            const double* __restrict__ sv = reinterpret_cast<const double*>(side_vp[F.r0]);
+        if (F.big) {  // its entries are copied into C after this kernel (k_big_copy)
             if (tid == 0) crp[F.r0 + 1] = base + agg;
-            for (int64_t q0 = 0; q0 < agg; q0 += 4 * NT) {
-                int32_t c4[4];
-                double v4[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int64_t q = q0 + u * NT + tid;
-                    if (q < agg) {
-                        c4[u] = sc[q];
-                        v4[u] = sv[q];
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int64_t q = q0 + u * NT + tid;
-                    if (q < agg) {
-                        ccol[base + q] = c4[u];
-                        cval[base + q] = v4[u];
-                    }
-                }
-            }
         } else {
             for (int t = tid; t < F.R; t += NT) crp[F.r0 + t + 1] = base + S.rend[t];
             tile_copy_out(S, nnz, base, ccol, cval, tid);
@@ -1850,6 +1863,7 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
         SPG_CUDA(cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem)));
         ctx->tile_attr_set = true;
     }
+    DBuf<int32_t> drows(ctx, nbig ? nbig : 1);
     if (nbig) {
         KTime kt(ctx, "big_rows");
         // the big rows (both lists), ascending, and their products
@@ -1859,7 +1873,6 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
                                  ctx->stream));
         SPG_CUDA(cudaStreamSynchronize(ctx->stream));
         std::sort(hrows.begin(), hrows.end());
-        DBuf<int32_t> drows(ctx, nbig);
         DBuf<int64_t> dprod(ctx, nbig);
         SPG_CUDA(cudaMemcpyAsync(drows.get(), hrows.data(), nbig * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
         k_side_gather<<<grid_for(ctx, nbig), 256, 0, ctx->stream>>>(drows, nbig, prod, dprod);
@@ -1968,6 +1981,12 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
         k_tile<<<grid, tile::NT, sizeof(TileSmem), ctx->stream>>>(a->rowptr, a->values, espan, b->colind, b->values,
                                                                   tr, te, ntiles, ticket, cshift, side_cp, side_vp,
                                                                   side_nnz, status, c->rowptr, c->colind, c->values);
+        SPG_LAUNCH_CHECK();
+    }
+    if (nbig) {
+        KTime kt(ctx, "big_copy");
+        k_big_copy<<<std::min(nbig, ctx->num_sms * 8), 256, 0, ctx->stream>>>(drows, nbig, side_cp, side_vp,
+                                                                             c->rowptr, c->colind, c->values);
         SPG_LAUNCH_CHECK();
     }
     hprof.mark("launch_tile");

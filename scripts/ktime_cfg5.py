@@ -23,3 +23,21 @@ dev.synchronize()
 print(f"config5 wall/step {1e3 * (time.perf_counter() - t0) / 3:.2f} ms nnz {nnz}")
 for k, (n, ms) in sorted(dev.timing_read().items()):
     print(f"   {k:20s} {ms / max(n, 1):10.3f} ms x{n}")
+
+try:  # phase profile when built with -DSPG_TILE_PROF
+    import ctypes as C
+    from paper_2603_21444_b200 import _capi
+    f = _capi.lib().spg_dev_tile_prof
+    buf = (C.c_ulonglong * 16)()
+    f(buf)
+    c = dev.spgemm(da, db)
+    dev.synchronize()
+    f(buf)
+    names = ["loop-top", "process(rest)", "publish+sync", "prologue(rest)", "gather-issue", "look-back",
+             "crp+copy-out", "final sync", "p:mul+count", "p:count barrier", "p:scan", "p:place",
+             "p:place barrier", "p:pairs+lists", "p:or-barrier", "pro:loads"]
+    tot = sum(buf[i] for i in range(16)) or 1
+    for i, nm in enumerate(names):
+        print(f"      {nm:20s} {100 * buf[i] / tot:5.1f}%")
+except AttributeError:
+    pass
