@@ -957,14 +957,10 @@ __global__ void k_tile_scatter(const int64_t* __restrict__ flag, const int64_t* 
     }
 }
 
-// side_off[row] / side_nnz[row] of the BIG rows from their list order.
+// per-row values of the BIG rows in their list order.
 __global__ void k_side_gather(const int32_t* __restrict__ rows, int n, const int64_t* __restrict__ rnnz,
                               int64_t* __restrict__ out) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) out[t] = rnnz[rows[t]];
-}
-__global__ void k_side_scatter(const int32_t* __restrict__ rows, int n, const int64_t* __restrict__ off,
-                               int64_t* __restrict__ side_off) {
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) side_off[rows[t]] = off[t];
 }
 
 // ------------------------------------------------- BIG rows: sort-based ESC
@@ -1142,8 +1138,8 @@ struct __align__(16) TileSmem {
     int32_t re[tile::RMAX + 1];    // first entry of each row (relative to the tile)
     int32_t rend[tile::RMAX];      // end of each row in the (compacted) staging
     uint32_t list[tile::LMAX];     // shared buckets of >= 3 products: start | end << 16
-    uint32_t hbm[tile::HW];        // duplicate path: head bitmap
-    int32_t hpre[tile::HW];        //   and its word prefix
+    uint32_t dbm[tile::HW];        // duplicates: staged entries that repeat their predecessor's (row, column)
+    int32_t dpre[tile::HW];        //   and the word prefix of their count
     uint16_t xs[tile::PMAX];       // product id of a staged entry of a shared bucket
     uint16_t eof[tile::PMAX];      // entry of each product
     int32_t ws[4][tile::NW];       // scan workspaces (rotated)
@@ -1160,9 +1156,9 @@ struct TileDesc {
     bool big;
 };
 
-// Number of heads (distinct (row, column) runs) before staging position q.
-__device__ __forceinline__ int head_prefix(const TileSmem& S, int q) {
-    return S.hpre[q >> 5] + __popc(S.hbm[q >> 5] & ((1u << (q & 31)) - 1u));
+// Number of duplicate entries before staging position q.
+__device__ __forceinline__ int dups_before(const TileSmem& S, int q) {
+    return S.dpre[q >> 5] + __popc(S.dbm[q >> 5] & ((1u << (q & 31)) - 1u));
 }
 
 // Contiguous smem -> global copy of n staged entries to C[base, base+n) with
@@ -1324,6 +1320,8 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
             aux[j] = static_cast<int>((atomicAdd(&S.cnt[b >> 1], 1u << sh) >> sh) & 0xffffu);
         }
     }
+    // duplicate bitmap of this tile (the previous tile's was consumed by its copy-out)
+    for (int q = tid; q < (ptile >> 5) + 2; q += NT) S.dbm[q] = 0u;
     TPROF(8)
     __syncthreads();
     TPROF(9)
@@ -1403,10 +1401,13 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
             const int32_t oc = S.col[other];
             const int ox = S.xs[other];
             const int x = tid + NT * j;
-            dup |= oc == col[j];
             const int fpos = pos - slot + ((oc < col[j] || (oc == col[j] && ox < x)) ? 1 : 0);
             if (fpos != pos) S.col[fpos] = col[j];
             S.val[fpos] = val[j];
+            if (oc == col[j]) {  // equal columns: the larger product id repeats the smaller
+                dup = true;
+                if (ox < x) atomicOr(&S.dbm[fpos >> 5], 1u << (fpos & 31));
+            }
         }
     }
     const int nlist = S.nlist;
@@ -1427,7 +1428,11 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
             S.xs[c + 1] = xa;
             S.val[c + 1] = va;
         }
-        for (int a = lo + 1; a < hi; ++a) dup |= S.col[a] == S.col[a - 1];
+        for (int a = lo + 1; a < hi; ++a)
+            if (S.col[a] == S.col[a - 1]) {
+                dup = true;
+                atomicOr(&S.dbm[a >> 5], 1u << (a & 31));
+            }
     }
     TPROF(13)
     const int anydup = __syncthreads_or(dup);
@@ -1436,54 +1441,53 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
         for (int t = tid; t < T.R; t += NT) S.rend[t] = S.epre[S.re[t + 1]];
         return ptile;
     }
-    // duplicates: combine runs of equal (row, column) in product-id order
-    // (= ascending k), compacting the staging in place
+    // duplicates (equal (row, column); rare): the ranking marked every staged
+    // entry that repeats its predecessor; their word prefix (one warp) gives
+    // every head its compacted position. Runs are folded in product-id order
+    // = ascending k.
     const int hw = (ptile >> 5) + 1;
-    for (int q = tid; q < hw + 1; q += NT) S.hbm[q] = 0u;
-    __syncthreads();
-    for (int t = tid; t < T.R; t += NT) {  // row starts are heads
-        const int ps = S.epre[S.re[t]];
-        if (S.epre[S.re[t + 1]] > ps) atomicOr(&S.hbm[ps >> 5], 1u << (ps & 31));
-    }
-    __syncthreads();
+    if (warp == 0) {
+        constexpr int PW = (tile::HW + 31) / 32;
+        int c[PW], sum = 0;
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-        const int x = tid + NT * j;  // a warp covers one bitmap word
-        bool head = false;
-        if (x < ptile) head = ((S.hbm[x >> 5] >> (x & 31)) & 1u) || x == 0 || S.col[x] != S.col[x - 1];
-        const unsigned hm = __ballot_sync(0xffffffffu, head);
-        __syncwarp();
-        if (lane == 0 && (warp * 32 + NT * j) < ptile) S.hbm[x >> 5] = hm;
+        for (int u = 0; u < PW; ++u) {
+            const int w = lane * PW + u;
+            c[u] = w < hw ? __popc(S.dbm[w]) : 0;
+            sum += c[u];
+        }
+        int pre = warp_inclusive_scan(sum) - sum;
+#pragma unroll
+        for (int u = 0; u < PW; ++u) {
+            const int w = lane * PW + u;
+            if (w < tile::HW) S.dpre[w] = pre;
+            pre += c[u];
+        }
     }
     __syncthreads();
-    int nnz;
-    {
-        const int v = tid < hw ? __popc(S.hbm[tid]) : 0;
-        const int hp = tile_scan(v, &nnz, S.ws[2]);
-        if (tid < hw) S.hpre[tid] = hp;
-        if (tid == 0) S.hpre[hw] = nnz;
-    }
-    __syncthreads();
-    int32_t oc[NJ];
+    // fold each run into its head and move the heads down (two phases: all
+    // reads, a barrier, all writes), so the copy-out stays one contiguous run
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
         const int x = tid + NT * j;
         aux[j] = -1;
-        oc[j] = 0;
-        if (x < ptile && ((S.hbm[x >> 5] >> (x & 31)) & 1u)) {
-            aux[j] = head_prefix(S, x);
-            oc[j] = S.col[x];
-            double s = S.val[x];
-            for (int u = x + 1; u < ptile && !((S.hbm[u >> 5] >> (u & 31)) & 1u); ++u) s = dadd(s, S.val[u]);
-            val[j] = s;
+        if (x < ptile && !((S.dbm[x >> 5] >> (x & 31)) & 1u)) {
+            double v = S.val[x];
+            for (int u = x + 1; u < ptile && ((S.dbm[u >> 5] >> (u & 31)) & 1u); ++u) v = dadd(v, S.val[u]);
+            aux[j] = x - dups_before(S, x);
+            col[j] = S.col[x];
+            val[j] = v;
         }
     }
-    for (int t = tid; t < T.R; t += NT) S.rend[t] = head_prefix(S, S.epre[S.re[t + 1]]);
+    for (int t = tid; t < T.R; t += NT) {
+        const int pe = S.epre[S.re[t + 1]];
+        S.rend[t] = pe - dups_before(S, pe);
+    }
+    const int nnz = ptile - dups_before(S, ptile);
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < NJ; ++j)
         if (aux[j] >= 0) {
-            S.col[aux[j]] = oc[j];
+            S.col[aux[j]] = col[j];
             S.val[aux[j]] = val[j];
         }
     return nnz;
@@ -1845,7 +1849,7 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     hprof.mark("launch1");
     SPG_CUDA(cudaStreamSynchronize(ctx->stream));
     hprof.mark("sync1");
-    const int ncta = hc[0], nheavy = hc[1], nside = ncta + nheavy;
+    const int ncta = hc[0], nheavy = hc[1];
 
     // 3: BIG rows: sort-based ESC in batches bounded by products
     const int nbig = ncta + nheavy;
@@ -1864,6 +1868,7 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
         ctx->tile_attr_set = true;
     }
     DBuf<int32_t> drows(ctx, nbig ? nbig : 1);
+    int64_t big_products = 0, big_nnz = 0;  // C capacity = products of tile rows + exact nnz of big rows
     if (nbig) {
         KTime kt(ctx, "big_rows");
         // the big rows (both lists), ascending, and their products
@@ -1884,6 +1889,7 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
         while ((int64_t(1) << colbits) < n) ++colbits;
         int64_t bmax = int64_t(300) << 20;  // products per batch (~48 B of workspace each)
         for (int64_t v : hp) bmax = std::max(bmax, v);
+        for (int64_t v : hp) big_products += v;
         std::vector<int> cut{0};  // batches of consecutive big rows
         for (int64_t r = 0, acc = 0; r < nbig; ++r) {
             if (r > cut.back() && acc + hp[r] > bmax) {
@@ -1936,6 +1942,7 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
                 exclusive_scan_i64(ctx, flagb, posb, P);
                 total = read_scalar(ctx, posb.get() + P);
             }
+            big_nnz += total;
             outc.emplace_back(new DBuf<int32_t>(ctx, total));
             outv.emplace_back(new DBuf<double>(ctx, total));
             hprof.mark("big_scan");
@@ -1970,7 +1977,7 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     SPG_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned long long), ctx->stream));
     spg_csr* c = new_csr(ctx, m, n, -1);
     hprof.mark("tilesetup");
-    alloc_c_arrays(ctx, c, products);  // upper bound of nnz(C)
+    alloc_c_arrays(ctx, c, products - big_products + big_nnz);  // upper bound of nnz(C)
     hprof.mark("allocC");
     SPG_CUDA(cudaMemsetAsync(c->rowptr, 0, sizeof(int64_t), ctx->stream));
     int occ = 1;
