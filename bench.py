@@ -181,7 +181,7 @@ def reference_arm(args):
               f"reference spgemm_local (oracle/_ref, csr.cpp:132-165), 1 thread each; gen {gen_s:.1f}s")
     line = {
         "metric": METRIC, "value": round(gflops, 4), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_per, 3), "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": round(ms_per, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference gen_erdos_renyi, seed 1)",
         "impl": "reference",
         "config": {"workload": CONFIGS[args.config]["desc"], "config_id": args.config, "n": n,
@@ -312,7 +312,7 @@ def ours_single(args):
     cpu = cpu_baseline_sample(a) if os.environ.get("SPG_SKIP_CPU") != "1" else None
     line = {
         "metric": METRIC, "value": round(gflops, 3), "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference gen_erdos_renyi, seed 1)",
         "config": {"workload": CONFIGS[args.config]["desc"], "config_id": args.config, "grid": "P=1 lambda=1 q=1",
                    "products": products, "nnz_A": nnz_a, "nnz_C": nnz_c,
@@ -423,12 +423,23 @@ def ours_multi(args):
     for x in (c_rp, c_ci, c_va):
         _capi.check(L.spg_host_register(x.ctypes.data, x.nbytes))
 
+    dbg = os.environ.get("SPG_BENCH_DEBUG")
+    phase = np.zeros(3)
+
     def e2e_step():
+        t0 = time.perf_counter()
         ex.reload(at_h, bt_h)
+        if dbg:
+            dev.synchronize()
+        t1 = time.perf_counter()
         dist.barrier()
         c, _ = ex.trident_step(procs, lam, grid.q)
+        if dbg:
+            dev.synchronize()
+        t2 = time.perf_counter()
         _capi.check(L.spg_csr_download(dev.ctx, c.h, c_rp.ctypes.data, c_ci.ctypes.data, 4, c_va.ctypes.data))
         c.free()
+        phase[:] += (t1 - t0, t2 - t1, time.perf_counter() - t2)
 
     e2e_steps = max(1, min(args.steps, int(os.environ.get("SPG_E2E_STEPS", 3))))
     e2e_step()
@@ -438,6 +449,9 @@ def ours_multi(args):
         e2e_step()
     dev.synchronize()
     e2e_local = (time.perf_counter() - t0) / e2e_steps * 1e3
+    if dbg:
+        print(f"[rank {rank}] e2e ms {e2e_local:.2f} (h2d, step, d2h) ms {np.round(phase / (e2e_steps + 1) * 1e3, 2).tolist()} "
+              f"cpu affinity {sorted(os.sched_getaffinity(0))[:4]}.. of {len(os.sched_getaffinity(0))}", file=sys.stderr, flush=True)
     et = torch.tensor([e2e_local], dtype=torch.float64, device=f"cuda:{local}")
     dist.all_reduce(et, op=dist.ReduceOp.MAX)
     e2e_ms = float(et.item())

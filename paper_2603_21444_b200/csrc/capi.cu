@@ -115,6 +115,8 @@ spg_status spg_init(int device, spg_ctx** out) {
         ctx->device = device;
         ctx->num_sms = prop.multiProcessorCount;
         ctx->l2_bytes = prop.l2CacheSize;
+        ctx->mem_total = prop.totalGlobalMem;
+        ctx_live(device, 1);
         const char* tp = std::getenv("SPG_TWO_PASS");
         ctx->two_pass = (tp && tp[0] == '1') ? 1 : 0;
         SPG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
@@ -155,6 +157,7 @@ spg_status spg_finalize(spg_ctx* ctx) {
         if (!ctx) return;
         DeviceScope ds(ctx->device);
         big_cache_release(ctx);
+        ctx_live(ctx->device, -1);
         cudaStreamSynchronize(ctx->stream);
         for (auto& r : ctx->timer.pending) {
             cudaEventDestroy(r.start);

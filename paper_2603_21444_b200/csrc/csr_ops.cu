@@ -4,6 +4,7 @@
 //   extract  (reference partition.cpp:161-222, one tile)
 //   column_normalize / prune (reference csr.cpp:224-249) — MCL post-step
 //   check_canonical (reference csr.cpp:30-50)
+#include <atomic>
 #include <algorithm>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -181,7 +182,6 @@ __global__ void k_extract_copy(const int64_t* __restrict__ beg, const int64_t* _
 // Column sums in CSR storage order (reference csr.cpp:225-227): entries are
 // stably radix-sorted by column (value as payload), then each column is summed
 // sequentially in storage order, so sums are bit-identical.
-__global__ void k_iota_i64(int64_t* p, int64_t n) { GRID_STRIDE(i, n) p[i] = i; }
 
 __global__ void k_colsum_runs(const int32_t* __restrict__ keys, const double* __restrict__ sval, int64_t nnz,
                               double* __restrict__ colsum) {
@@ -292,9 +292,17 @@ spg_csr* new_csr(spg_ctx* ctx, int64_t nrows, int64_t ncols, int64_t nnz) {
 
 namespace {
 constexpr size_t BIG_ROUND = size_t(64) << 20;
-constexpr size_t BIG_KEEP = 48;                        // cached blocks per context
-constexpr size_t BIG_KEEP_BYTES = size_t(32) << 30;    // and at most this many bytes
+constexpr size_t BIG_KEEP = 48;  // cached blocks per context
+std::atomic<int> g_live[64];     // live contexts per device
+// at most this many bytes per context: 45% of device memory shared among the
+// device's live contexts (at least 16 GB)
+size_t big_keep_bytes(const spg_ctx* ctx) {
+    const int live = std::max(1, g_live[ctx->device & 63].load());
+    return std::max(size_t(16) << 30, static_cast<size_t>(0.45 * static_cast<double>(ctx->mem_total)) / live);
+}
 }  // namespace
+
+void ctx_live(int device, int delta) { g_live[device & 63] += delta; }
 
 void* pool_alloc(spg_ctx* ctx, size_t bytes) {
     void* p = nullptr;
@@ -346,7 +354,8 @@ void big_free(spg_ctx* ctx, void* p, size_t cap) {
     ctx->big_cache.emplace_back(p, cap);
     size_t held = 0;
     for (auto& b : ctx->big_cache) held += b.second;
-    while (held > BIG_KEEP_BYTES && ctx->big_cache.size() > 1) {  // drop the oldest
+    const size_t keep = big_keep_bytes(ctx);
+    while (held > keep && ctx->big_cache.size() > 1) {  // drop the oldest
         held -= ctx->big_cache.front().second;
         cudaFreeAsync(ctx->big_cache.front().first, ctx->stream);
         ctx->big_cache.erase(ctx->big_cache.begin());

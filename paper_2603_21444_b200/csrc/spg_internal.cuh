@@ -75,6 +75,7 @@ struct spg_ctx {
     // the pool splits freed blocks for smaller requests, after which a
     // multi-GB request maps fresh memory on every call (see big_alloc).
     std::vector<std::pair<void*, size_t>> big_cache;
+    size_t mem_total = 0;  // device memory (sizes the block cache)
     int two_pass = 0;  // 1: symbolic + numeric warp kernels instead of the single-pass tiles (SPG_TWO_PASS=1)
 };
 
@@ -167,6 +168,8 @@ void free_csr(spg_csr* m);
 // colind/values of a new product with room for `cap` entries (big arrays via the block cache).
 void alloc_c_arrays(spg_ctx* ctx, spg_csr* c, int64_t cap);
 void big_cache_release(spg_ctx* ctx);
+// live contexts per device (the block cache's byte budget is shared among them)
+void ctx_live(int device, int delta);
 int64_t read_scalar(spg_ctx* ctx, const int64_t* dptr);
 
 // Kernels (spgemm.cu / spgeam.cu / misc.cu)

@@ -36,6 +36,10 @@
 #include "block_scan.cuh"
 #include "spg_internal.cuh"
 
+#ifndef SPG_K32_COLBITS
+#define SPG_K32_COLBITS 24  // 32-bit sort keys for the BIG rows up to this many column bits
+#endif
+
 namespace spgb {
 namespace {
 
@@ -957,6 +961,12 @@ __global__ void k_tile_scatter(const int64_t* __restrict__ flag, const int64_t* 
     }
 }
 
+// entries of the listed rows of A
+__global__ void k_row_nnz(const int32_t* __restrict__ rows, int n, const int64_t* __restrict__ arp,
+                          int64_t* __restrict__ out) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+        out[t] = arp[rows[t] + 1] - arp[rows[t]];
+}
 // per-row values of the BIG rows in their list order.
 __global__ void k_side_gather(const int32_t* __restrict__ rows, int n, const int64_t* __restrict__ rnnz,
                               int64_t* __restrict__ out) {
@@ -971,85 +981,194 @@ __global__ void k_side_gather(const int32_t* __restrict__ rows, int n, const int
 // stable sort keeps a run in product order = ascending k, so the sums are
 // bit-identical to the reference's acc[j] += av*bv.
 
-// CTA per big row: entries in chunks of NT (block scan of lengths), then the
-// warps copy the chunk's B rows (lanes over a row) to their product slots.
-__global__ void __launch_bounds__(256) k_big_expand(const int32_t* __restrict__ rows, int nrows,
-                                                    const int64_t* __restrict__ off, const int64_t* __restrict__ arp,
-                                                    const int32_t* __restrict__ acol, const double* __restrict__ aval,
-                                                    const int64_t* __restrict__ brp, const int32_t* __restrict__ bcol,
-                                                    const double* __restrict__ bval, int colbits,
-                                                    uint64_t* __restrict__ keys, double* __restrict__ vals) {
-    __shared__ int64_t s_bs[256], s_pre[257];
-    __shared__ double s_av[256];
-    __shared__ int32_t ws[9];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// Expansion of a batch, balanced by products (one R-MAT row can hold 3.6e7
+// of them): k_big_ent lists the batch's A entries (B row start, B row
+// length, A value, row in batch) in row order; a scan of the lengths gives
+// every entry its first product; k_big_fill then takes chunks of FILL_CH
+// consecutive products, marks where each entry starts inside the chunk,
+// propagates the entry id with a max-scan and writes every product as
+// (row-in-batch << colbits | column, av*bv) — product order within a row is
+// ascending k, which the stable sort keeps.
+// K = uint32_t when row-in-batch and column bits fit 32 (a third less sort
+// traffic), else uint64_t.
+__global__ void __launch_bounds__(256) k_big_ent(const int32_t* __restrict__ rows, int nrows,
+                                                 const int64_t* __restrict__ eoff, const int64_t* __restrict__ arp,
+                                                 const int32_t* __restrict__ acol, const double* __restrict__ aval,
+                                                 const int64_t* __restrict__ brp, int64_t* __restrict__ eb,
+                                                 int64_t* __restrict__ elen, double* __restrict__ eav,
+                                                 int32_t* __restrict__ erow) {
     for (int r = blockIdx.x; r < nrows; r += gridDim.x) {
-        const int64_t i = rows[r];
-        const int64_t ea = arp[i], eb = arp[i + 1];
-        int64_t base = off[r];
-        const uint64_t rk = static_cast<uint64_t>(r) << colbits;
-        for (int64_t c = ea; c < eb; c += 256) {
-            const int64_t e = c + tid;
-            int len = 0;
-            if (e < eb) {
-                const int32_t k = acol[e];
-                s_bs[tid] = brp[k];
-                len = static_cast<int>(brp[k + 1] - s_bs[tid]);
-                s_av[tid] = aval[e];
-            }
-            int total;
-            const int pre = block_exclusive_scan<256>(len, &total, ws);
-            s_pre[tid] = pre;
-            if (tid == 0) s_pre[256] = total;
-            __syncthreads();
-            const int n = static_cast<int>(min(int64_t(256), eb - c));
-            for (int q = warp; q < n; q += 8) {
-                const int64_t bs = s_bs[q];
-                const int l = static_cast<int>(s_pre[q + 1] - s_pre[q]);
-                const double av = s_av[q];
-                const int64_t o = base + s_pre[q];
-                for (int x = lane; x < l; x += 32) {
-                    keys[o + x] = rk | static_cast<uint32_t>(bcol[bs + x]);
-                    vals[o + x] = dmul(av, bval[bs + x]);
-                }
-            }
-            base += total;
-            __syncthreads();
+        const int64_t i = rows[r], ea = arp[i], ne = arp[i + 1] - ea, g0 = eoff[r];
+        for (int64_t t = threadIdx.x; t < ne; t += blockDim.x) {
+            const int32_t k = acol[ea + t];
+            const int64_t bs = brp[k];
+            eb[g0 + t] = bs;
+            elen[g0 + t] = brp[k + 1] - bs;
+            eav[g0 + t] = aval[ea + t];
+            erow[g0 + t] = r;
         }
     }
 }
 
-// flag[i] = 1 at the first element of each run of equal keys.
-__global__ void k_big_heads(const uint64_t* __restrict__ keys, int64_t n, int64_t* __restrict__ flag) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
-        flag[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
-}
+constexpr int FILL_CH = 4096, FILL_IT = FILL_CH / 256;
 
-// One thread per run head: the run's sum in product order.
-__global__ void k_big_runs(const uint64_t* __restrict__ keys, const double* __restrict__ vals, int64_t n,
-                           const int64_t* __restrict__ pos, int colbits, int32_t* __restrict__ ocol,
-                           double* __restrict__ oval) {
-    const uint64_t cmask = (uint64_t(1) << colbits) - 1;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const uint64_t k = keys[i];
-        if (i > 0 && keys[i - 1] == k) continue;
-        double s = dadd(0.0, vals[i]);
-        for (int64_t u = i + 1; u < n && keys[u] == k; ++u) s = dadd(s, vals[u]);
-        const int64_t o = pos[i];
-        ocol[o] = static_cast<int32_t>(k & cmask);
-        oval[o] = s;
+template <typename K>
+__global__ void __launch_bounds__(256) k_big_fill(const int64_t* __restrict__ pst, int64_t E,
+                                                  const int64_t* __restrict__ eb, const double* __restrict__ eav,
+                                                  const int32_t* __restrict__ erow, const int32_t* __restrict__ bcol,
+                                                  const double* __restrict__ bval, int colbits, int64_t P,
+                                                  K* __restrict__ keys, double* __restrict__ vals) {
+    __shared__ int32_t mark[FILL_CH];
+    __shared__ int32_t ws[9];
+    __shared__ int64_t s_lo;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int64_t c = blockIdx.x; c * FILL_CH < P; c += gridDim.x) {
+        const int64_t P0 = c * FILL_CH;
+        const int n = static_cast<int>(min(int64_t(FILL_CH), P - P0));
+        if (tid == 0) {  // the entry holding product P0: the last g with pst[g] <= P0
+            int64_t lo = 0, hi = E - 1;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi + 1) >> 1;
+                if (pst[mid] <= P0) lo = mid;
+                else hi = mid - 1;
+            }
+            s_lo = lo;
+        }
+        for (int x = tid; x < FILL_CH; x += 256) mark[x] = -1;
+        __syncthreads();
+        const int64_t glo = s_lo;
+        if (tid == 0) mark[0] = static_cast<int32_t>(glo);
+        // entries starting inside the chunk; among entries sharing a start
+        // only the last can have products, so the largest id wins
+        for (int64_t g = glo + 1 + tid; g < E; g += 256) {
+            const int64_t p = pst[g];
+            if (p >= P0 + n) break;
+            atomicMax(&mark[p - P0], static_cast<int32_t>(g));
+        }
+        __syncthreads();
+        // inclusive max-scan of mark (thread t owns [t*FILL_IT, (t+1)*FILL_IT))
+        int32_t m[FILL_IT], run = -1;
+#pragma unroll
+        for (int u = 0; u < FILL_IT; ++u) {
+            m[u] = mark[tid * FILL_IT + u];
+            run = max(run, m[u]);
+        }
+        int32_t inc = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc = max(inc, y);
+        }
+        if (lane == 31) ws[warp] = inc;
+        __syncthreads();
+        int32_t carry = -1;
+        for (int w = 0; w < warp; ++w) carry = max(carry, ws[w]);
+        int32_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
+        if (lane == 0) ex = -1;
+        carry = max(carry, ex);
+#pragma unroll
+        for (int u = 0; u < FILL_IT; ++u) {
+            carry = max(carry, m[u]);
+            mark[tid * FILL_IT + u] = carry;
+        }
+        __syncthreads();
+        for (int x = tid; x < n; x += 256) {
+            const int32_t g = mark[x];
+            const int64_t u = eb[g] + (P0 + x - pst[g]);
+            keys[P0 + x] = (static_cast<K>(erow[g]) << colbits) | static_cast<K>(static_cast<uint32_t>(bcol[u]));
+            vals[P0 + x] = dmul(eav[g], bval[u]);
+        }
+        __syncthreads();
     }
 }
 
-// Per big row of the batch: its sorted products are [off[r], off[r+1]) of the
-// batch (keys start with the row), so its output is [pos[off[r]], pos[off[r+1]]).
-__global__ void k_big_finish(const int32_t* __restrict__ rows, int nrows, const int64_t* __restrict__ off,
-                             const int64_t* __restrict__ pos, const int32_t* ocol, const double* oval,
-                             uint64_t* __restrict__ side_cp, uint64_t* __restrict__ side_vp,
-                             int64_t* __restrict__ side_nnz) {
+// Runs of equal keys in the sorted batch, in chunks of RUN_CH elements (each
+// thread owns RUN_IT consecutive ones): k_run_count counts the run heads per
+// chunk; after a scan of the counts k_run_sum gives every head its output slot
+// and sums its run sequentially (product order = ascending k, so the sum is
+// bit-identical to the reference's acc[j] += av*bv), and records where each
+// row of the batch starts in the output.
+constexpr int RUN_IT = 16, RUN_CH = 256 * RUN_IT;
+
+// Loads the RUN_IT keys owned by the thread at i0 (16-byte loads when the
+// chunk is full: i0 is a multiple of RUN_IT and the buffer 256-byte aligned)
+// and returns the mask of run heads among them.
+template <typename K>
+__device__ __forceinline__ uint32_t run_heads(const K* __restrict__ keys, int64_t n, int64_t i0, K (&k)[RUN_IT]) {
+    if (i0 >= n) return 0;
+    if (i0 + RUN_IT <= n) {
+        constexpr int PER = 16 / sizeof(K);
+#pragma unroll
+        for (int u = 0; u < RUN_IT / PER; ++u) {
+            const uint4 w = __ldg(reinterpret_cast<const uint4*>(keys + i0) + u);
+            memcpy(&k[u * PER], &w, 16);
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < RUN_IT; ++u) k[u] = i0 + u < n ? keys[i0 + u] : K(0);
+    }
+    K prev = i0 > 0 ? keys[i0 - 1] : ~k[0];
+    uint32_t hm = 0;
+#pragma unroll
+    for (int u = 0; u < RUN_IT; ++u) {
+        if (i0 + u < n && k[u] != prev) hm |= 1u << u;
+        prev = k[u];
+    }
+    return hm;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(256) k_run_count(const K* __restrict__ keys, int64_t n, int64_t* __restrict__ cnt) {
+    __shared__ int ws[9];
+    const int64_t nch = (n + RUN_CH - 1) / RUN_CH;
+    for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+        K k[RUN_IT];
+        const int h = __popc(run_heads(keys, n, ch * RUN_CH + int64_t(threadIdx.x) * RUN_IT, k));
+        int total;
+        block_exclusive_scan<256>(h, &total, ws);
+        if (threadIdx.x == 0) cnt[ch] = total;
+    }
+}
+
+// Each head sums its run sequentially from memory (runs are short except
+// for hub columns, where one thread walks the run and the others skip).
+template <typename K>
+__global__ void __launch_bounds__(256) k_run_sum(const K* __restrict__ keys, const double* __restrict__ vals, int64_t n,
+                                                 const int64_t* __restrict__ cbase, int colbits,
+                                                 int32_t* __restrict__ ocol, double* __restrict__ oval,
+                                                 int64_t* __restrict__ rowstart) {
+    __shared__ int ws[9];
+    const K cmask = (K(1) << colbits) - 1;
+    const int64_t nch = (n + RUN_CH - 1) / RUN_CH;
+    for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+        const int64_t i0 = ch * RUN_CH + int64_t(threadIdx.x) * RUN_IT;
+        K k[RUN_IT];
+        uint32_t hm = run_heads(keys, n, i0, k);
+        int total;
+        int64_t o = cbase[ch] + block_exclusive_scan<256>(__popc(hm), &total, ws);
+        while (hm) {
+            const int u = __ffs(hm) - 1;
+            hm &= hm - 1;
+            const int64_t i = i0 + u;
+            const K key = keys[i];
+            double sum = dadd(0.0, vals[i]);
+            for (int64_t v = i + 1; v < n && keys[v] == key; ++v) sum = dadd(sum, vals[v]);
+            ocol[o] = static_cast<int32_t>(key & cmask);
+            oval[o] = sum;
+            if (i == 0 || (keys[i - 1] >> colbits) != (key >> colbits)) rowstart[key >> colbits] = o;
+            ++o;
+        }
+    }
+}
+
+// Per big row of the batch: its output is [rowstart[r], rowstart[r+1]) (every
+// big row has products, so every row starts a run; rowstart[nrows] = total).
+__global__ void k_big_finish(const int32_t* __restrict__ rows, int nrows, const int64_t* __restrict__ rowstart,
+                             int64_t total, const int32_t* ocol, const double* oval, uint64_t* __restrict__ side_cp,
+                             uint64_t* __restrict__ side_vp, int64_t* __restrict__ side_nnz) {
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
         const int64_t i = rows[r];
-        const int64_t f = pos[off[r]], l = pos[off[r + 1]];
+        const int64_t f = rowstart[r], l = r + 1 < nrows ? rowstart[r + 1] : total;
         side_cp[i] = reinterpret_cast<uint64_t>(ocol + f);
         side_vp[i] = reinterpret_cast<uint64_t>(oval + f);
         side_nnz[i] = l - f;
@@ -1880,80 +1999,130 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
         std::sort(hrows.begin(), hrows.end());
         DBuf<int64_t> dprod(ctx, nbig);
         SPG_CUDA(cudaMemcpyAsync(drows.get(), hrows.data(), nbig * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+        DBuf<int64_t> dne(ctx, nbig);
         k_side_gather<<<grid_for(ctx, nbig), 256, 0, ctx->stream>>>(drows, nbig, prod, dprod);
         SPG_LAUNCH_CHECK();
-        std::vector<int64_t> hp(nbig);
+        k_row_nnz<<<grid_for(ctx, nbig), 256, 0, ctx->stream>>>(drows, nbig, a->rowptr, dne);
+        SPG_LAUNCH_CHECK();
+        std::vector<int64_t> hp(nbig), hne(nbig);
         SPG_CUDA(cudaMemcpyAsync(hp.data(), dprod.get(), nbig * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        SPG_CUDA(cudaMemcpyAsync(hne.data(), dne.get(), nbig * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
         SPG_CUDA(cudaStreamSynchronize(ctx->stream));
         int colbits = 1;
         while ((int64_t(1) << colbits) < n) ++colbits;
-        int64_t bmax = int64_t(300) << 20;  // products per batch (~48 B of workspace each)
+        // 32-bit sort keys when the row-in-batch bits fit beside the column bits
+        const bool k32 = colbits <= SPG_K32_COLBITS;
+        const int64_t rows_cap = k32 ? (int64_t(1) << (32 - colbits)) : (int64_t(1) << 30);
+        int64_t bmax = int64_t(400) << 20;  // products per batch (~24-32 B of workspace each)
         for (int64_t v : hp) bmax = std::max(bmax, v);
         for (int64_t v : hp) big_products += v;
         std::vector<int> cut{0};  // batches of consecutive big rows
-        for (int64_t r = 0, acc = 0; r < nbig; ++r) {
-            if (r > cut.back() && acc + hp[r] > bmax) {
+        for (int64_t r = 0, acc = 0, eacc = 0; r < nbig; ++r) {  // entry ids of a batch fit int32
+            if (r > cut.back() &&
+                (acc + hp[r] > bmax || r - cut.back() >= rows_cap || eacc + hne[r] > (int64_t(1) << 30))) {
                 cut.push_back(static_cast<int>(r));
-                acc = 0;
+                acc = eacc = 0;
             }
             acc += hp[r];
+            eacc += hne[r];
         }
         cut.push_back(nbig);
-        int64_t pmax = 0;
+        int64_t pmax = 0, nbmax = 0, emax = 0;
         for (size_t t = 0; t + 1 < cut.size(); ++t) {
-            int64_t P = 0;
-            for (int r = cut[t]; r < cut[t + 1]; ++r) P += hp[r];
+            int64_t P = 0, E = 0;
+            for (int r = cut[t]; r < cut[t + 1]; ++r) P += hp[r], E += hne[r];
             pmax = std::max(pmax, P);
+            emax = std::max(emax, E);
+            nbmax = std::max<int64_t>(nbmax, cut[t + 1] - cut[t]);
         }
-        DBuf<uint64_t> keys(ctx, pmax), keys2(ctx, pmax);
+        DBuf<int64_t> eb(ctx, emax), elen(ctx, emax), pst(ctx, emax + 1), deoff(ctx, nbmax + 1);
+        DBuf<double> eav(ctx, emax);
+        DBuf<int32_t> erow(ctx, emax);
+        std::vector<int64_t> heoff(nbmax + 1);
+        const size_t kb = k32 ? 4 : 8;
+        DBuf<unsigned char> keys(ctx, pmax * kb), keys2(ctx, pmax * kb);
         DBuf<double> vals(ctx, pmax), vals2(ctx, pmax);
-        DBuf<int64_t> flagb(ctx, pmax), posb(ctx, pmax + 1), doff(ctx, nbig + 1);
+        const int64_t nchmax = (pmax + RUN_CH - 1) / RUN_CH;
+        DBuf<int64_t> ccnt(ctx, nchmax + 1), cbase(ctx, nchmax + 1), rstart(ctx, nbmax + 1);
         size_t tmp_bytes = 0;
-        SPG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.get(), keys2.get(), vals.get(), vals2.get(),
-                                                 std::max<int64_t>(pmax, 1), 0, 64, ctx->stream));
+        if (k32)
+            SPG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (uint32_t*)keys.get(), (uint32_t*)keys2.get(),
+                                                     vals.get(), vals2.get(), std::max<int64_t>(pmax, 1), 0, 32,
+                                                     ctx->stream));
+        else
+            SPG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (uint64_t*)keys.get(), (uint64_t*)keys2.get(),
+                                                     vals.get(), vals2.get(), std::max<int64_t>(pmax, 1), 0, 64,
+                                                     ctx->stream));
         DBuf<unsigned char> tmp(ctx, tmp_bytes);
         std::vector<int64_t> hoff(nbig + 1);
         for (size_t t = 0; t + 1 < cut.size(); ++t) {
             const int r0 = cut[t], nb = cut[t + 1] - cut[t];
             hoff[0] = 0;
             for (int r = 0; r < nb; ++r) hoff[r + 1] = hoff[r] + hp[r0 + r];
-            const int64_t P = hoff[nb];
-            SPG_CUDA(cudaMemcpyAsync(doff.get(), hoff.data(), (nb + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
+            const int64_t P = hoff[nb];  // > 0: big rows have products
+            heoff[0] = 0;
+            for (int r = 0; r < nb; ++r) heoff[r + 1] = heoff[r] + hne[r0 + r];
+            const int64_t E = heoff[nb];
+            SPG_CUDA(cudaMemcpyAsync(deoff.get(), heoff.data(), (nb + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
                                      ctx->stream));
             int rowbits = 1;
             while ((int64_t(1) << rowbits) < nb) ++rowbits;
-            int64_t total = 0;
+            const int64_t nch = (P + RUN_CH - 1) / RUN_CH;
+            const int rgrid = static_cast<int>(std::min<int64_t>(nch, int64_t(ctx->num_sms) * 8));
             hprof.mark("big_batch_setup");
-            if (P > 0) {
+            {
                 KTime kx(ctx, "big_expand");
-                k_big_expand<<<std::min(nb, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
-                    drows.get() + r0, nb, doff, a->rowptr, a->colind, a->values, b->rowptr, b->colind, b->values,
-                    colbits, keys, vals);
+                k_big_ent<<<std::min(nb, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+                    drows.get() + r0, nb, deoff, a->rowptr, a->colind, a->values, b->rowptr, eb, elen, eav, erow);
+                SPG_LAUNCH_CHECK();
+                exclusive_scan_i64(ctx, elen, pst, E);
+                const int fgrid = static_cast<int>(std::min<int64_t>((P + FILL_CH - 1) / FILL_CH, ctx->num_sms * 8));
+                if (k32)
+                    k_big_fill<uint32_t><<<fgrid, 256, 0, ctx->stream>>>(pst, E, eb, eav, erow, b->colind, b->values,
+                                                                         colbits, P, (uint32_t*)keys.get(), vals);
+                else
+                    k_big_fill<uint64_t><<<fgrid, 256, 0, ctx->stream>>>(pst, E, eb, eav, erow, b->colind, b->values,
+                                                                         colbits, P, (uint64_t*)keys.get(), vals);
                 SPG_LAUNCH_CHECK();
             }
-            if (P > 0) {
+            {
                 KTime ks(ctx, "big_sort");
-                SPG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tmp_bytes, keys.get(), keys2.get(), vals.get(),
-                                                         vals2.get(), P, 0, colbits + rowbits, ctx->stream));
+                if (k32)
+                    SPG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tmp_bytes, (uint32_t*)keys.get(),
+                                                             (uint32_t*)keys2.get(), vals.get(), vals2.get(), P, 0,
+                                                             colbits + rowbits, ctx->stream));
+                else
+                    SPG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tmp_bytes, (uint64_t*)keys.get(),
+                                                             (uint64_t*)keys2.get(), vals.get(), vals2.get(), P, 0,
+                                                             colbits + rowbits, ctx->stream));
             }
-            if (P > 0) {
-                k_big_heads<<<grid_for(ctx, P), 256, 0, ctx->stream>>>(keys2, P, flagb);
+            {
+                KTime kc(ctx, "big_count");
+                if (k32)
+                    k_run_count<uint32_t><<<rgrid, 256, 0, ctx->stream>>>((uint32_t*)keys2.get(), P, ccnt);
+                else
+                    k_run_count<uint64_t><<<rgrid, 256, 0, ctx->stream>>>((uint64_t*)keys2.get(), P, ccnt);
                 SPG_LAUNCH_CHECK();
-                exclusive_scan_i64(ctx, flagb, posb, P);
-                total = read_scalar(ctx, posb.get() + P);
+                exclusive_scan_i64(ctx, ccnt, cbase, nch);
             }
+            const int64_t total = read_scalar(ctx, cbase.get() + nch);
             big_nnz += total;
             outc.emplace_back(new DBuf<int32_t>(ctx, total));
             outv.emplace_back(new DBuf<double>(ctx, total));
             hprof.mark("big_scan");
-            if (P > 0) {
+            {
                 KTime kr(ctx, "big_runs");
-                k_big_runs<<<grid_for(ctx, P), 256, 0, ctx->stream>>>(keys2, vals2, P, posb, colbits,
-                                                                       outc.back()->get(), outv.back()->get());
+                if (k32)
+                    k_run_sum<uint32_t><<<rgrid, 256, 0, ctx->stream>>>((uint32_t*)keys2.get(), vals2, P, cbase,
+                                                                        colbits, outc.back()->get(),
+                                                                        outv.back()->get(), rstart);
+                else
+                    k_run_sum<uint64_t><<<rgrid, 256, 0, ctx->stream>>>((uint64_t*)keys2.get(), vals2, P, cbase,
+                                                                        colbits, outc.back()->get(),
+                                                                        outv.back()->get(), rstart);
                 SPG_LAUNCH_CHECK();
             }
-            if (P == 0) SPG_CUDA(cudaMemsetAsync(posb.get(), 0, sizeof(int64_t), ctx->stream));
-            k_big_finish<<<grid_for(ctx, nb), 256, 0, ctx->stream>>>(drows.get() + r0, nb, doff, posb,
+            k_big_finish<<<grid_for(ctx, nb), 256, 0, ctx->stream>>>(drows.get() + r0, nb, rstart, total,
                                                                      outc.back()->get(), outv.back()->get(), side_cp,
                                                                      side_vp, side_nnz);
             SPG_LAUNCH_CHECK();

@@ -1,4 +1,5 @@
-"""Per-kernel times of C = A*A on R-MAT(scale) (dev tool)."""
+"""Per-kernel times of C = A*A on R-MAT(scale) (dev tool).
+usage: ktime_rmat.py SCALE [ROW0 ROW1]  (a row range of A times A: scale 22 does not fit whole)"""
 import sys
 import time
 sys.path.insert(0, ".")
@@ -15,15 +16,20 @@ print(f"scale {s}: n={a.nrows} nnz={a.nnz} products={rp.sum()} rows>512: {(rp > 
       f" prod in >4096: {rp[rp > 4096].sum()} in 513..4096: {rp[(rp > 512) & (rp <= 4096)].sum()} max ne {ne.max()}")
 dev = spg.Device(0)
 da = dev.upload(a)
+dl = da
+if len(sys.argv) > 3:
+    r0, r1 = int(sys.argv[2]), int(sys.argv[3])
+    dl = dev.extract(da, r0, r1, 0, int(a.ncols))
+    print(f"rows {r0}..{r1}: products {rp[r0:r1].sum()}")
 dev.timing(True)
-c = dev.spgemm(da, da)
+c = dev.spgemm(dl, da)
 dev.synchronize()
 dev.timing_reset()
 reps = 3
 t0 = time.perf_counter()
 for _ in range(reps):
     del c
-    c = dev.spgemm(da, da)
+    c = dev.spgemm(dl, da)
     dev.synchronize()
 print(f"wall {1e3 * (time.perf_counter() - t0) / reps:.1f} ms/step nnzC={c.nnz}")
 for k, (n, ms) in sorted(dev.timing_read().items()):
