@@ -124,7 +124,8 @@ spg_status spg_csr_extract(spg_ctx* ctx, const spg_csr* m, int64_t r0, int64_t r
 spg_status spg_csr_copy(spg_ctx* ctx, const spg_csr* m, spg_csr** out);
 
 /* Host-buffer convenience for the drop-in path: upload A and B, multiply,
- * keep C on the device (query with spg_csr_shape, fetch with spg_csr_download). */
+ * keep C on the device (query with spg_csr_shape, fetch with spg_csr_download).
+ * When B's host arrays are A's (C = A*A) the matrix is uploaded once. */
 spg_status spg_spgemm_host(spg_ctx* ctx, int64_t a_nrows, int64_t a_ncols, const int64_t* a_rowptr,
                            const void* a_colind, const double* a_values, int64_t b_nrows, int64_t b_ncols,
                            const int64_t* b_rowptr, const void* b_colind, const double* b_values,

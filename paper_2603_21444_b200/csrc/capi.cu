@@ -428,9 +428,13 @@ spg_status spg_spgemm_host(spg_ctx* ctx, int64_t a_nrows, int64_t a_ncols, const
                            const int64_t* b_rowptr, const void* b_colind, const double* b_values, int colind_width,
                            spg_csr** c) {
     spg_csr *a = nullptr, *b = nullptr;
+    // C = A*A (the same host matrix passed twice) uploads it once
+    const bool same = a_nrows == b_nrows && a_ncols == b_ncols && a_rowptr == b_rowptr && a_colind == b_colind &&
+                      a_values == b_values;
     spg_status st = spg_csr_upload(ctx, a_nrows, a_ncols, a_rowptr, a_colind, colind_width, a_values, &a);
-    if (st == SPG_OK) st = spg_csr_upload(ctx, b_nrows, b_ncols, b_rowptr, b_colind, colind_width, b_values, &b);
-    if (st == SPG_OK) st = spg_spgemm(ctx, a, b, c);
+    if (st == SPG_OK && !same)
+        st = spg_csr_upload(ctx, b_nrows, b_ncols, b_rowptr, b_colind, colind_width, b_values, &b);
+    if (st == SPG_OK) st = spg_spgemm(ctx, a, same ? a : b, c);
     if (a) spg_csr_free(a);
     if (b) spg_csr_free(b);
     return st;

@@ -1,5 +1,5 @@
-timeout 900 python bench.py > gpurun_out/bench_n1.json 2> gpurun_out/bench_n1.err; tail -c 600 gpurun_out/bench_n1.json
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; tail -1 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py > gpurun_out/bench_n1.json 2> gpurun_out/bench_n1.err; tail -c 700 gpurun_out/bench_n1.json
 SPG_SKIP_CPU=1 SPG_E2E_STEPS=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 > gpurun_out/ncu_launch.log 2>&1; tail -1 gpurun_out/ncu_launch.log
 timeout 900 ncu --set full --import-source on --clock-control none -k k_tile --launch-count 1 -o gpurun_out/k_tile_full -f python scripts/probe_small.py 4194304 16 1 > gpurun_out/ncu_full.log 2>&1; tail -1 gpurun_out/ncu_full.log
-timeout 900 python scripts/configs.py --configs 1,2,4,5 > gpurun_out/configs.jsonl 2> gpurun_out/configs.err
-timeout 900 python scripts/configs.py --configs 3 --rmat-scale 18 >> gpurun_out/configs.jsonl 2>> gpurun_out/configs.err; cat gpurun_out/configs.jsonl
+timeout 900 python scripts/configs.py --configs 1,2,4,5 > gpurun_out/configs.jsonl 2> gpurun_out/configs.err; cat gpurun_out/configs.jsonl

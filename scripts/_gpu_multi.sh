@@ -1,2 +1,3 @@
 N=${N:-2}
-SPG_BENCH_DEBUG=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus $N --steps 10 --warmup 3 > gpurun_out/bench_n$N.json 2> gpurun_out/bench_n$N.err; tail -c 400 gpurun_out/bench_n$N.json; grep "rank" gpurun_out/bench_n$N.err | tail -4 | cut -c1-200
+SPG_BENCH_DEBUG=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus $N --steps 10 --warmup 3 > gpurun_out/bench_n$N.json 2> gpurun_out/bench_n$N.err; tail -c 400 gpurun_out/bench_n$N.json; grep "rank" gpurun_out/bench_n$N.err | tail -8 | cut -c1-200
+if [ "$REF" = 1 ]; then timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; tail -c 400 gpurun_out/bench_ref.json; fi

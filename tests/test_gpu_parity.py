@@ -252,3 +252,27 @@ def test_trident_rectangular_kmer_shape():
     r = spg.trident_spgemm(a, at, spg.TridentGrid.create(8, 2))
     c = O.port_spgemm(a, at)
     assert spg.pattern_equal(r.c, c) and spg.allclose(r.c, c, REL_TOL)
+
+
+@pytest.mark.parametrize("shared", [True, False])
+def test_spgemm_host_entry(dev, shared):
+    """spg_spgemm_host (host buffers in, C on the device): C = A*A with the same
+    host arrays passed twice (uploaded once) and C = A*B with distinct ones."""
+    import ctypes as C
+    from paper_2603_21444_b200 import _capi
+    L = _capi.lib()
+    a = O.port_gen_erdos_renyi(3000, 0.004, 11)
+    b = a if shared else O.port_gen_erdos_renyi(3000, 0.004, 12)
+    arrs = []
+    for m in (a, b):
+        arrs.append((np.ascontiguousarray(m.rowptr, np.int64), np.ascontiguousarray(np.asarray(m.colind), np.int32),
+                     np.ascontiguousarray(m.values, np.float64)))
+    if shared:
+        arrs[1] = arrs[0]
+    (arp, aci, ava), (brp, bci, bva) = arrs
+    h = C.c_void_p()
+    _capi.check(L.spg_spgemm_host(dev.ctx, int(a.nrows), int(a.ncols), arp.ctypes.data, aci.ctypes.data,
+                                  ava.ctypes.data, int(b.nrows), int(b.ncols), brp.ctypes.data, bci.ctypes.data,
+                                  bva.ctypes.data, 4, C.byref(h)))
+    c = spg.DeviceCsr(dev, h.value).download()
+    assert same(c, O.port_spgemm(a, b))
