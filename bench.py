@@ -348,9 +348,22 @@ def ours_multi(args):
     from paper_2603_21444_b200 import dist as sd
 
     rank, world, local = env_rank()
+    # SPG_OVERSUBSCRIBE=1 (functional check of the N=8 path on a smaller box):
+    # ranks share GPUs round-robin and the plumbing runs on gloo, since NCCL
+    # refuses two ranks on one device. Timings of such a run mean nothing.
+    over = os.environ.get("SPG_OVERSUBSCRIBE") == "1"
+    if over:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if over:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    tdev = "cpu" if over else f"cuda:{local}"
     procs, lam = sd.grid_for_gpus(world)
+    if os.environ.get("SPG_GRID"):  # experiment: another legal grid for this world size, "P,lambda"
+        procs, lam = (int(x) for x in os.environ["SPG_GRID"].split(","))
+        assert procs == world, "SPG_GRID must have P = number of ranks"
     grid = spg.TridentGrid.create(procs, lam)
     a = make_input(args.config)
     dev = spg.Device(local)
@@ -370,7 +383,7 @@ def ours_multi(args):
         da = dev.upload(a)
         products_total = dev.products(da, da)
         del da
-    pt = torch.tensor([products_total], dtype=torch.int64, device=f"cuda:{local}")
+    pt = torch.tensor([products_total], dtype=torch.int64, device=tdev)
     dist.broadcast(pt, 0)
     products_total = int(pt.item())
 
@@ -395,12 +408,12 @@ def ours_multi(args):
         ev1.record(stream)
         ev1.synchronize()
     ms_local = ev0.elapsed_time(ev1) / args.steps
-    t = torch.tensor([ms_local], dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor([ms_local], dtype=torch.float64, device=tdev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     kt = dev.timing_read()
     launches = sum(v[0] for v in kt.values())
-    lt = torch.tensor([launches], dtype=torch.int64, device=f"cuda:{local}")
+    lt = torch.tensor([launches], dtype=torch.int64, device=tdev)
     dist.all_reduce(lt)
     # end to end through the public API with HOST buffers: every step each rank
     # refills its tiles from pinned host memory (H2D), the ranks run the trident
@@ -452,12 +465,12 @@ def ours_multi(args):
     if dbg:
         print(f"[rank {rank}] e2e ms {e2e_local:.2f} (h2d, step, d2h) ms {np.round(phase / (e2e_steps + 1) * 1e3, 2).tolist()} "
               f"cpu affinity {sorted(os.sched_getaffinity(0))[:4]}.. of {len(os.sched_getaffinity(0))}", file=sys.stderr, flush=True)
-    et = torch.tensor([e2e_local], dtype=torch.float64, device=f"cuda:{local}")
+    et = torch.tensor([e2e_local], dtype=torch.float64, device=tdev)
     dist.all_reduce(et, op=dist.ReduceOp.MAX)
     e2e_ms = float(et.item())
     h2d = sum(x.nbytes for x in at_h + bt_h)
     d2h = c_rp.nbytes + nnz_c * 12
-    hb = torch.tensor([h2d, d2h], dtype=torch.int64, device=f"cuda:{local}")
+    hb = torch.tensor([h2d, d2h], dtype=torch.int64, device=tdev)
     dist.all_reduce(hb)
     for x in at_h + bt_h + (c_rp, c_ci, c_va):
         L.spg_host_unregister(x.ctypes.data)

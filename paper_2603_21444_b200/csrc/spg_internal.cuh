@@ -177,6 +177,8 @@ spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b);
 int64_t spgemm_products(spg_ctx* ctx, const spg_csr* a, const spg_csr* b);
 spg_csr* spgeam(spg_ctx* ctx, const spg_csr* a, const spg_csr* b);
 spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n);
+// [A_0 | A_1 | ...] of row-aligned parts (at most 16)
+spg_csr* hconcat(spg_ctx* ctx, const spg_csr* const* parts, int n);
 spg_csr* extract(spg_ctx* ctx, const spg_csr* m, int64_t r0, int64_t r1, int64_t c0, int64_t c1);
 spg_csr* copy_csr(spg_ctx* ctx, const spg_csr* m);
 void column_normalize(spg_ctx* ctx, spg_csr* m);

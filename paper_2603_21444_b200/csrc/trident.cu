@@ -17,6 +17,7 @@
 // Round r+1's pulls are issued on a copy stream before round r's multiply, so
 // the NVLink transfer overlaps the multiply (double buffering).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -120,6 +121,7 @@ namespace {
 struct RoundPlan {
     int a_owner;
     std::vector<int> b_owners;  // slices of the B block, in row order
+    int s = 0;                  // the k block of the round (A column block, B row block)
 };
 
 struct EvPair {
@@ -134,9 +136,80 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 
 // Runs all rounds of one rank on its context. `views[t]` are handles to every
 // owner's tile readable from this device (local, peer or IPC-mapped).
+// q >= 2 rounds as ONE multiply: the rounds' A tiles side by side in k order,
+// [A_{i,0,k} | A_{i,1,k} | ...], times their B blocks stacked in the same
+// order. Every C entry is then summed over ascending global k in one pass —
+// bit-identical to the serial reference spgemm_local — and the partial-C
+// merges (the reference's spgeam per round, algorithms.cpp:82-90) disappear.
+// Every tile still moves exactly as the reference schedule moves it (same
+// ledger); the pulls of all rounds are issued together on the copy stream.
+spg_csr* run_rank_concat(spg_ctx* ctx, const std::vector<RoundPlan>& plan, const spg_csr* const* a_views,
+                         const spg_csr* const* b_views, double* tl) {
+    const int R = static_cast<int>(plan.size());
+    cudaStream_t cs = ctx->xfer;
+    spg_ctx cctx = *ctx;
+    cctx.stream = cs;
+    cctx.big_cache.clear();
+    cctx.timer = Timer{};
+    std::vector<int> ord(R);
+    for (int r = 0; r < R; ++r) ord[r] = r;
+    std::sort(ord.begin(), ord.end(), [&](int x, int y) { return plan[x].s < plan[y].s; });
+    cudaEvent_t f0 = ctx->timer.ev(), ready = ctx->timer.ev(), e0 = ctx->timer.ev(), e1 = ctx->timer.ev(),
+                e2 = ctx->timer.ev();
+    std::vector<spg_csr*> a_parts;
+    std::vector<bool> a_owned;
+    spg_csr *a_all = nullptr, *b_all = nullptr, *c = nullptr;
+    try {
+        SPG_CUDA(cudaEventRecord(f0, cs));
+        std::vector<const spg_csr*> bsl;
+        for (int r : ord) {
+            const spg_csr* av = a_views[plan[r].a_owner];
+            const bool local = av->ctx == ctx && av->storage != 2;
+            a_parts.push_back(local ? const_cast<spg_csr*>(av) : copy_csr(&cctx, av));
+            a_owned.push_back(!local);
+            for (int o : plan[r].b_owners) bsl.push_back(b_views[o]);
+        }
+        b_all = vconcat(&cctx, bsl.data(), static_cast<int>(bsl.size()));
+        SPG_CUDA(cudaEventRecord(ready, cs));
+        SPG_CUDA(cudaEventRecord(e0, ctx->stream));
+        SPG_CUDA(cudaStreamWaitEvent(ctx->stream, ready, 0));
+        SPG_CUDA(cudaEventRecord(e1, ctx->stream));
+        for (size_t p = 0; p < a_parts.size(); ++p)
+            if (a_owned[p]) a_parts[p]->ctx = ctx;  // freed on the compute stream below
+        b_all->ctx = ctx;
+        a_all = hconcat(ctx, a_parts.data(), R);
+        c = spgemm(ctx, a_all, b_all);
+        SPG_CUDA(cudaEventRecord(e2, ctx->stream));
+        free_csr(a_all);
+        free_csr(b_all);
+        for (size_t p = 0; p < a_parts.size(); ++p)
+            if (a_owned[p]) free_csr(a_parts[p]);
+        SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+        SPG_CUDA(cudaStreamSynchronize(cs));
+    } catch (...) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaStreamSynchronize(cs);
+        throw;
+    }
+    if (tl) {
+        for (int r = 0; r < R * 4; ++r) tl[r] = 0.0;
+        tl[0] = elapsed(f0, ready);  // pull every round's A tile + assemble B (copy stream)
+        tl[1] = elapsed(e0, e1);     // exposed wait for the exchange
+        tl[2] = elapsed(e1, e2);     // hconcat of the A tiles + local multiply
+    }
+    for (auto e : {f0, ready, e0, e1, e2}) ctx->timer.pool.push_back(e);
+    big_cache_release(&cctx);
+    return c;
+}
+
 spg_csr* run_rank(spg_ctx* ctx, const std::vector<RoundPlan>& plan, const spg_csr* const* a_views,
                   const spg_csr* const* b_views, int64_t c_rows, int64_t c_cols, double* tl /* rounds*4 */) {
     DeviceScope ds(ctx->device);
+    // SPG_ROUND_MERGE=1: the reference's structure (multiply per round, merge
+    // the partial C tiles), kept for comparison
+    const char* me = std::getenv("SPG_ROUND_MERGE");
+    const bool merge_rounds = me && me[0] == '1';
+    if (plan.size() > 1 && plan.size() <= 16 && !merge_rounds) return run_rank_concat(ctx, plan, a_views, b_views, tl);
     cudaStream_t cs = ctx->xfer;  // persistent transfer stream of the context
     spg_ctx cctx = *ctx;  // same device and pool, copy stream
     cctx.stream = cs;
@@ -249,6 +322,7 @@ std::vector<RoundPlan> trident_plan(const GridInfo& g, int rank) {
     for (int r = 0; r < g.q; ++r) {
         const int s = (r + i + j) % g.q;
         plan[r].a_owner = g.rank_of(i, s, k);
+        plan[r].s = s;
         for (int k2 = 0; k2 < g.lam; ++k2) plan[r].b_owners.push_back(g.rank_of(s, j, k2));
     }
     return plan;
@@ -376,6 +450,7 @@ spg_status spg_summa_spgemm(spg_ctx* const* ctxs, int nctx, const spg_csr* const
                 for (int r = 0; r < pr; ++r) {
                     plan[r].a_owner = i * pr + r;
                     plan[r].b_owners = {r * pr + j};
+                    plan[r].s = r;
                 }
                 out[rank] = run_rank(ctxs[rank % nctx], plan, a_tiles, b_tiles, a_tiles[rank]->nrows,
                                      b_tiles[j]->ncols, timeline_out ? timeline_out + size_t(rank) * pr * 4 : nullptr);

@@ -224,13 +224,22 @@ def test_determinism(dev):
     assert same(c1, c2)
 
 
+@pytest.mark.parametrize("merge", [False, True])
 @pytest.mark.parametrize("P,lam", [(1, 1), (2, 2), (4, 1), (4, 4), (8, 2), (16, 4)])
-def test_trident_parity_and_ledger(P, lam):
+def test_trident_parity_and_ledger(P, lam, merge, monkeypatch):
+    """Default: a rank's q rounds are one multiply of its A tiles side by side
+    (k order) times the stacked B blocks, so C is bit-identical to the serial
+    reference. SPG_ROUND_MERGE=1: the reference structure (multiply per round
+    + spgeam), within 1e-12 of the serial product like the reference's own."""
+    if merge:
+        monkeypatch.setenv("SPG_ROUND_MERGE", "1")
     a, b = csr("er300_p3_A"), csr("er300_p3_B")
     r = spg.trident_spgemm(a, b, spg.TridentGrid.create(P, lam))
     ref_c = csr("er300_p3_C")
     assert spg.pattern_equal(r.c, ref_c)
     assert spg.allclose(r.c, ref_c, REL_TOL)
+    if not merge:
+        assert same(r.c, ref_c)
     assert np.array_equal(r.c.values, z()[f"trident_P{P}_L{lam}_Cvalues"]) or spg.allclose(
         r.c, O.Csr(ref_c.nrows, ref_c.ncols, ref_c.rowptr, ref_c.colind, z()[f"trident_P{P}_L{lam}_Cvalues"]),
         REL_TOL)
@@ -243,6 +252,7 @@ def test_summa_parity_and_ledger(P):
     a, b = csr("er300_p3_A"), csr("er300_p3_B")
     r = spg.summa_spgemm(a, b, P, 2)
     assert spg.allclose(r.c, csr("er300_p3_C"), REL_TOL)
+    assert same(r.c, csr("er300_p3_C"))  # stages as one k-ordered multiply
     assert np.array_equal(r.ledger, z()[f"summa_P{P}_ledger"])
 
 
@@ -252,6 +262,7 @@ def test_trident_rectangular_kmer_shape():
     r = spg.trident_spgemm(a, at, spg.TridentGrid.create(8, 2))
     c = O.port_spgemm(a, at)
     assert spg.pattern_equal(r.c, c) and spg.allclose(r.c, c, REL_TOL)
+    assert same(r.c, c)
 
 
 @pytest.mark.parametrize("shared", [True, False])
