@@ -510,8 +510,12 @@ spg_csr* copy_csr(spg_ctx* ctx, const spg_csr* s) {
     return c;
 }
 
-spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n) {
-    if (n == 0) return new_csr(ctx, 0, 0, 0);
+spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n, cudaEvent_t rp_ready) {
+    if (n == 0) {
+        spg_csr* z = new_csr(ctx, 0, 0, 0);
+        if (rp_ready) SPG_CUDA(cudaEventRecord(rp_ready, ctx->stream));
+        return z;
+    }
     int64_t rows = 0, nnz = 0;
     const int64_t ncols = slices[0]->ncols;
     for (int s = 0; s < n; ++s) {
@@ -557,6 +561,7 @@ spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n) {
         r += sl->nrows;
         base += sl->nnz;
     }
+    if (rp_ready) SPG_CUDA(cudaEventRecord(rp_ready, ctx->stream));
     if (n > 1 && ctx->aux[0])
         for (int i = 0; i < std::min(n, spg_ctx::NAUX); ++i) {
             SPG_CUDA(cudaEventRecord(ctx->aux_ev[i], ctx->aux[i]));

@@ -173,10 +173,14 @@ void ctx_live(int device, int delta);
 int64_t read_scalar(spg_ctx* ctx, const int64_t* dptr);
 
 // Kernels (spgemm.cu / spgeam.cu / misc.cu)
-spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b);
+// b_data: when set, B's column/value arrays are complete only at this event
+// (its row pointers and A are ready): the symbolic preparation overlaps the pull.
+spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEvent_t b_data = nullptr);
 int64_t spgemm_products(spg_ctx* ctx, const spg_csr* a, const spg_csr* b);
 spg_csr* spgeam(spg_ctx* ctx, const spg_csr* a, const spg_csr* b);
-spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n);
+// rp_ready (optional): recorded once the row pointers are assembled; the
+// column/value pulls may still be running on the aux streams then.
+spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n, cudaEvent_t rp_ready = nullptr);
 // [A_0 | A_1 | ...] of row-aligned parts (at most 16)
 spg_csr* hconcat(spg_ctx* ctx, const spg_csr* const* parts, int n);
 spg_csr* extract(spg_ctx* ctx, const spg_csr* m, int64_t r0, int64_t r1, int64_t c0, int64_t c1);

@@ -1928,7 +1928,7 @@ struct HostProf {
 };
 
 // Single-pass tiled multiply (the default).
-spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
+spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEvent_t b_data) {
     HostProf hprof;
     const int64_t m = a->nrows, n = b->ncols;
     const int cshift = cshift_for(n);
@@ -1969,6 +1969,9 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     SPG_CUDA(cudaStreamSynchronize(ctx->stream));
     hprof.mark("sync1");
     const int ncta = hc[0], nheavy = hc[1];
+    // B's columns and values may still be arriving (trident pulls): everything
+    // above read only B's row pointers
+    if (b_data) SPG_CUDA(cudaStreamWaitEvent(ctx->stream, b_data, 0));
 
     // 3: BIG rows: sort-based ESC in batches bounded by products
     const int nbig = ncta + nheavy;
@@ -2181,16 +2184,19 @@ extern "C" int spg_dev_tile_prof(unsigned long long* out) {
 }
 #endif
 
-spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
+spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEvent_t b_data) {
     if (a->ncols != b->nrows)
         fail(SPG_DIMENSION_ERROR,
              "spgemm: a.ncols=" + std::to_string(a->ncols) + " != b.nrows=" + std::to_string(b->nrows));
     const int64_t m = a->nrows, n = b->ncols;
-    if (m == 0 || a->nnz == 0 || b->nnz == 0) return new_csr(ctx, m, n, 0);
     if (n > (int64_t(1) << 31)) fail(SPG_PARAMETER_ERROR, "spgemm: b.ncols must be < 2^31 (int32 column indices)");
+    const bool tiled = !(ctx->two_pass || b->nnz >= (int64_t(1) << tile::SP_BS));
+    if (b_data && (m == 0 || a->nnz == 0 || b->nnz == 0 || !tiled))
+        SPG_CUDA(cudaStreamWaitEvent(ctx->stream, b_data, 0));
+    if (m == 0 || a->nnz == 0 || b->nnz == 0) return new_csr(ctx, m, n, 0);
     // the tile path packs B row starts in 34 bits (always true on one GPU)
-    if (ctx->two_pass || b->nnz >= (int64_t(1) << tile::SP_BS)) return spgemm_two_pass(ctx, a, b);
-    return spgemm_tiled(ctx, a, b);
+    if (!tiled) return spgemm_two_pass(ctx, a, b);
+    return spgemm_tiled(ctx, a, b, b_data);
 }
 
 }  // namespace spgb

@@ -155,7 +155,7 @@ spg_csr* run_rank_concat(spg_ctx* ctx, const std::vector<RoundPlan>& plan, const
     for (int r = 0; r < R; ++r) ord[r] = r;
     std::sort(ord.begin(), ord.end(), [&](int x, int y) { return plan[x].s < plan[y].s; });
     cudaEvent_t f0 = ctx->timer.ev(), ready = ctx->timer.ev(), e0 = ctx->timer.ev(), e1 = ctx->timer.ev(),
-                e2 = ctx->timer.ev();
+                e2 = ctx->timer.ev(), rp_ready = ctx->timer.ev();
     std::vector<spg_csr*> a_parts;
     std::vector<bool> a_owned;
     spg_csr *a_all = nullptr, *b_all = nullptr, *c = nullptr;
@@ -169,16 +169,18 @@ spg_csr* run_rank_concat(spg_ctx* ctx, const std::vector<RoundPlan>& plan, const
             a_owned.push_back(!local);
             for (int o : plan[r].b_owners) bsl.push_back(b_views[o]);
         }
-        b_all = vconcat(&cctx, bsl.data(), static_cast<int>(bsl.size()));
+        b_all = vconcat(&cctx, bsl.data(), static_cast<int>(bsl.size()), rp_ready);
         SPG_CUDA(cudaEventRecord(ready, cs));
         SPG_CUDA(cudaEventRecord(e0, ctx->stream));
-        SPG_CUDA(cudaStreamWaitEvent(ctx->stream, ready, 0));
+        // A tiles and B's row pointers are in place: hconcat and the multiply's
+        // row preparation overlap the column/value pulls
+        SPG_CUDA(cudaStreamWaitEvent(ctx->stream, rp_ready, 0));
         SPG_CUDA(cudaEventRecord(e1, ctx->stream));
         for (size_t p = 0; p < a_parts.size(); ++p)
             if (a_owned[p]) a_parts[p]->ctx = ctx;  // freed on the compute stream below
         b_all->ctx = ctx;
         a_all = hconcat(ctx, a_parts.data(), R);
-        c = spgemm(ctx, a_all, b_all);
+        c = spgemm(ctx, a_all, b_all, ready);
         SPG_CUDA(cudaEventRecord(e2, ctx->stream));
         free_csr(a_all);
         free_csr(b_all);
@@ -194,10 +196,10 @@ spg_csr* run_rank_concat(spg_ctx* ctx, const std::vector<RoundPlan>& plan, const
     if (tl) {
         for (int r = 0; r < R * 4; ++r) tl[r] = 0.0;
         tl[0] = elapsed(f0, ready);  // pull every round's A tile + assemble B (copy stream)
-        tl[1] = elapsed(e0, e1);     // exposed wait for the exchange
-        tl[2] = elapsed(e1, e2);     // hconcat of the A tiles + local multiply
+        tl[1] = elapsed(e0, e1);     // exposed wait (A tiles + B row pointers)
+        tl[2] = elapsed(e1, e2);     // hconcat of the A tiles + local multiply (overlaps the B data pulls)
     }
-    for (auto e : {f0, ready, e0, e1, e2}) ctx->timer.pool.push_back(e);
+    for (auto e : {f0, ready, e0, e1, e2, rp_ready}) ctx->timer.pool.push_back(e);
     big_cache_release(&cctx);
     return c;
 }
@@ -218,9 +220,9 @@ spg_csr* run_rank(spg_ctx* ctx, const std::vector<RoundPlan>& plan, const spg_cs
     const int R = static_cast<int>(plan.size());
     std::vector<spg_csr*> a_in(R, nullptr), b_in(R, nullptr);
     std::vector<bool> a_owned(R, false), b_owned(R, false);
-    std::vector<cudaEvent_t> ready(R), e0(R), e1(R), e2(R), e3(R), f0(R);
+    std::vector<cudaEvent_t> ready(R), e0(R), e1(R), e2(R), e3(R), f0(R), rp(R);
     for (int r = 0; r < R; ++r) {  // events from the context's pool (returned below)
-        for (auto* e : {&ready[r], &e0[r], &e1[r], &e2[r], &e3[r], &f0[r]}) *e = ctx->timer.ev();
+        for (auto* e : {&ready[r], &e0[r], &e1[r], &e2[r], &e3[r], &f0[r], &rp[r]}) *e = ctx->timer.ev();
     }
     auto issue_fetch = [&](int r) {
         SPG_CUDA(cudaEventRecord(f0[r], cs));
@@ -236,9 +238,10 @@ spg_csr* run_rank(spg_ctx* ctx, const std::vector<RoundPlan>& plan, const spg_cs
         } else {
             std::vector<const spg_csr*> sl;
             for (int o : p.b_owners) sl.push_back(b_views[o]);
-            b_in[r] = vconcat(&cctx, sl.data(), static_cast<int>(sl.size()));
+            b_in[r] = vconcat(&cctx, sl.data(), static_cast<int>(sl.size()), rp[r]);
             b_owned[r] = true;
         }
+        if (!b_owned[r]) SPG_CUDA(cudaEventRecord(rp[r], cs));
         // Free on the compute stream once the multiply has consumed them.
         a_in[r]->ctx = a_owned[r] ? ctx : a_in[r]->ctx;
         b_in[r]->ctx = b_owned[r] ? ctx : b_in[r]->ctx;
@@ -250,9 +253,9 @@ spg_csr* run_rank(spg_ctx* ctx, const std::vector<RoundPlan>& plan, const spg_cs
         for (int r = 0; r < R; ++r) {
             if (r + 1 < R) issue_fetch(r + 1);  // overlaps this round's multiply
             SPG_CUDA(cudaEventRecord(e0[r], ctx->stream));
-            SPG_CUDA(cudaStreamWaitEvent(ctx->stream, ready[r], 0));
+            SPG_CUDA(cudaStreamWaitEvent(ctx->stream, rp[r], 0));  // A + B row pointers
             SPG_CUDA(cudaEventRecord(e1[r], ctx->stream));
-            spg_csr* cr = spgemm(ctx, a_in[r], b_in[r]);
+            spg_csr* cr = spgemm(ctx, a_in[r], b_in[r], ready[r]);  // waits for B's data after its row prep
             SPG_CUDA(cudaEventRecord(e2[r], ctx->stream));
             if (!acc) acc = cr;
             else {
@@ -277,11 +280,11 @@ spg_csr* run_rank(spg_ctx* ctx, const std::vector<RoundPlan>& plan, const spg_cs
     for (int r = 0; r < R; ++r) {
         if (tl) {
             tl[r * 4 + 0] = elapsed(f0[r], ready[r]);  // pull A + assemble B (copy stream)
-            tl[r * 4 + 1] = elapsed(e0[r], e1[r]);     // exposed wait for the exchange
-            tl[r * 4 + 2] = elapsed(e1[r], e2[r]);     // local multiply
+            tl[r * 4 + 1] = elapsed(e0[r], e1[r]);     // exposed wait (A + B row pointers)
+            tl[r * 4 + 2] = elapsed(e1[r], e2[r]);     // local multiply (overlaps the B data pulls)
             tl[r * 4 + 3] = elapsed(e2[r], e3[r]);     // partial-C merge
         }
-        for (auto e : {ready[r], e0[r], e1[r], e2[r], e3[r], f0[r]}) ctx->timer.pool.push_back(e);
+        for (auto e : {ready[r], e0[r], e1[r], e2[r], e3[r], f0[r], rp[r]}) ctx->timer.pool.push_back(e);
     }
     big_cache_release(&cctx);
     cudaStreamSynchronize(cs);
