@@ -1,11 +1,15 @@
-"""Per-kernel times of config 5 (k-mer A*A^T) (dev tool)."""
+"""Per-kernel times of config 5 (k-mer A*A^T), or config 2 with argument `er` (dev tool)."""
 import sys
 import time
 sys.path.insert(0, ".")
 import paper_2603_21444_b200 as spg  # noqa: E402
 
-a = spg.gen_erdos_renyi_rect(1 << 22, 1 << 18, 2.0 ** -16, 5)
-at = spg.transpose(a)
+if len(sys.argv) > 1 and sys.argv[1] == "er":  # config 2 instead
+    a = spg.gen_erdos_renyi(1 << 22, 16.0 / (1 << 22), 1)
+    at = a
+else:
+    a = spg.gen_erdos_renyi_rect(1 << 22, 1 << 18, 2.0 ** -16, 5)
+    at = spg.transpose(a)
 dev = spg.Device(0)
 da, db = dev.upload(a), dev.upload(at)
 dev.timing(True)
