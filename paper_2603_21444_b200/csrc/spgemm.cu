@@ -879,48 +879,93 @@ __global__ void k_row_prep(const int64_t* __restrict__ arp, const int32_t* __res
                            const int64_t* __restrict__ brp, int64_t m, int64_t* __restrict__ prod,
                            int64_t* __restrict__ wt, int8_t* __restrict__ kind, uint64_t* __restrict__ espan,
                            int32_t* __restrict__ lists, int32_t* __restrict__ counts) {
-    const int lane = threadIdx.x & 31;
+    // half-warp per row (two rows in flight per warp: the row is a chain of
+    // dependent loads arp -> acol -> brp); loops are warp-uniform
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, sub = lane & 15, half = lane >> 4;
     const int64_t gw = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
     const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t i = gw; i < m; i += nw) {
-        const int64_t e0 = arp[i], e1 = arp[i + 1];
+    for (int64_t i0 = 2 * gw; i0 < m; i0 += 2 * nw) {
+        const int64_t i = i0 + half;
+        const bool ok = i < m;
+        int64_t e0 = 0, e1 = 0;
+        if (ok) {
+            e0 = arp[i];
+            e1 = arp[i + 1];
+        }
         const int64_t ne = e1 - e0;
-        int64_t p = 0, maxlen = 0;
-        for (int64_t eb = e0; eb < e1; eb += 32) {  // warp-uniform trip count
-            const int64_t e = eb + lane;
-            int64_t len = 0;
-            if (e < e1) {
-                const int32_t k = __ldg(acol + e);
-                len = __ldg(brp + k + 1) - __ldg(brp + k);
+        const int64_t ne_max = max(ne, static_cast<int64_t>(__shfl_xor_sync(FULL, ne, 16)));
+        int64_t p = 0, maxlen = 0, bsr[2] = {0, 0}, lenr[2] = {0, 0};  // rows of <= 32 entries keep their spans
+        for (int64_t t = 0; t < ne_max; t += 16) {
+            int64_t bs = 0, len = 0;
+            if (t + sub < ne) {
+                const int32_t k = __ldg(acol + e0 + t + sub);
+                bs = __ldg(brp + k);
+                len = __ldg(brp + k + 1) - bs;
             }
-            p += warp_reduce_sum(len);
+            if (t == 0) {  // (the other half's row may take more iterations)
+                bsr[0] = bs;
+                lenr[0] = len;
+            } else if (t == 16) {
+                bsr[1] = bs;
+                lenr[1] = len;
+            }
+            int64_t sum = len;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+            p += sum;
             maxlen = max(maxlen, len);
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+        for (int o = 8; o > 0; o >>= 1) maxlen = max(maxlen, static_cast<int64_t>(__shfl_xor_sync(FULL, maxlen, o)));
         int8_t rk = RK_BIG;
         if (tile_small(p, ne)) rk = RK_SMALL;
         else if (tile_weight(p, ne) <= tile::PMAX && maxlen <= tile::SP_LEN_MAX) rk = RK_MEDIUM;
-        if (rk != RK_BIG) {  // second pass: in-row product offsets -> espan
-            const uint64_t pr = static_cast<uint64_t>(p);
+        const uint64_t pr = static_cast<uint64_t>(p);
+        const bool spans = ok && rk != RK_BIG;
+        {  // rows of <= 32 entries: in-row product offsets from registers
             int64_t carry = 0;
-            for (int64_t eb = e0; eb < e1; eb += 32) {
-                const int64_t e = eb + lane;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                int64_t inc = lenr[c];
+#pragma unroll
+                for (int o = 1; o < 16; o <<= 1) {
+                    const int64_t y = __shfl_up_sync(FULL, inc, o, 16);
+                    if (sub >= o) inc += y;
+                }
+                if (spans && ne <= 32 && 16 * c + sub < ne)
+                    espan[e0 + 16 * c + sub] = (static_cast<uint64_t>(bsr[c]) & tile::SP_BS_MASK) |
+                                               (static_cast<uint64_t>(lenr[c]) << tile::SP_LEN) |
+                                               (static_cast<uint64_t>(carry + inc - lenr[c]) << tile::SP_IN) |
+                                               (pr << tile::SP_PR);
+                carry += __shfl_sync(FULL, inc, 15, 16);
+            }
+        }
+        const bool slow = spans && ne > 32;
+        if (__any_sync(FULL, slow)) {  // longer rows: a second pass
+            int64_t carry = 0;
+            for (int64_t t = 0; t < ne_max; t += 16) {
                 int64_t bs = 0, len = 0;
-                if (e < e1) {
-                    const int32_t k = __ldg(acol + e);
+                if (slow && t + sub < ne) {
+                    const int32_t k = __ldg(acol + e0 + t + sub);
                     bs = __ldg(brp + k);
                     len = __ldg(brp + k + 1) - bs;
                 }
-                const int64_t inc = warp_inclusive_scan(len);
-                if (e < e1)
-                    espan[e] = (static_cast<uint64_t>(bs) & tile::SP_BS_MASK) |
-                               (static_cast<uint64_t>(len) << tile::SP_LEN) |
-                               (static_cast<uint64_t>(carry + inc - len) << tile::SP_IN) | (pr << tile::SP_PR);
-                carry += __shfl_sync(0xffffffffu, inc, 31);
+                int64_t inc = len;
+#pragma unroll
+                for (int o = 1; o < 16; o <<= 1) {
+                    const int64_t y = __shfl_up_sync(FULL, inc, o, 16);
+                    if (sub >= o) inc += y;
+                }
+                if (slow && t + sub < ne)
+                    espan[e0 + t + sub] = (static_cast<uint64_t>(bs) & tile::SP_BS_MASK) |
+                                          (static_cast<uint64_t>(len) << tile::SP_LEN) |
+                                          (static_cast<uint64_t>(carry + inc - len) << tile::SP_IN) |
+                                          (pr << tile::SP_PR);
+                carry += __shfl_sync(FULL, inc, 15, 16);
             }
         }
-        if (lane == 0) {
+        if (ok && sub == 0) {
             prod[i] = p;
             kind[i] = rk;
             wt[i] = rk == RK_SMALL ? tile_weight(p, ne) : 0;
