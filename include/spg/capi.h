@@ -123,6 +123,28 @@ spg_status spg_csr_extract(spg_ctx* ctx, const spg_csr* m, int64_t r0, int64_t r
 /* Copy a handle (possibly from another device) into this context. */
 spg_status spg_csr_copy(spg_ctx* ctx, const spg_csr* m, spg_csr** out);
 
+/* Device tile store. Schemes as spgsim::Scheme (partition.hpp:10). */
+typedef enum spg_scheme { SPG_SCHEME_TRIDENT = 0, SPG_SCHEME_GRID2D = 1, SPG_SCHEME_ROWS1D = 2 } spg_scheme;
+/* The tile rectangles of make_tile_map (partition.cpp:95-159): rects_out
+ * receives procs x {row_begin, row_end, col_begin, col_end}. SPG_GRID_ERROR as
+ * the reference (trident: P % lambda, P/lambda a perfect square; grid2d: P a
+ * perfect square). */
+spg_status spg_tile_rects(int64_t nrows, int64_t ncols, int scheme, int procs, int gpus_per_node,
+                          int64_t* rects_out);
+/* Device partition (partition.cpp:161-222): the global matrix m, resident on
+ * its context's device, split into the procs tiles of make_tile_map with local
+ * indices. Tile r is built on ctxs[r % nctx] by kernels that read m in place
+ * (NVLink peer loads when m lives on another device): one pass over m, no host
+ * round trip. tiles_out receives procs handles. */
+spg_status spg_partition(spg_ctx* const* ctxs, int nctx, const spg_csr* m, int scheme, int procs, int gpus_per_node,
+                         spg_csr** tiles_out);
+/* Device reassemble (partition.cpp:224-261): the global nrows x ncols matrix
+ * from the procs tiles of that map (rank order, on any devices, read in place),
+ * built on ctx. SPG_INCOMPLETE_TILE_SET when the tile count or a tile's shape
+ * does not match the map. Bit-identical inverse of spg_partition. */
+spg_status spg_reassemble(spg_ctx* ctx, const spg_csr* const* tiles, int ntiles, int64_t nrows, int64_t ncols,
+                          int scheme, int procs, int gpus_per_node, spg_csr** out);
+
 /* Host-buffer convenience for the drop-in path: upload A and B, multiply,
  * keep C on the device (query with spg_csr_shape, fetch with spg_csr_download).
  * When B's host arrays are A's (C = A*A) the matrix is uploaded once. */

@@ -224,6 +224,25 @@ class Device:
     def copy(self, m: DeviceCsr) -> DeviceCsr:
         return self._out(_capi.lib().spg_csr_copy, m.h)
 
+    def partition(self, m: DeviceCsr, scheme: str, procs: int, gpus_per_node: int, devices=None):
+        """Device tile store: partition.cpp:161-222 on the GPU (spg_partition).
+        m lives on this device; tile r is built on devices[r % len(devices)]
+        (default: this device). -> (tiles, TileMap)."""
+        devs = list(devices) if devices else [self]
+        ctxs = (C.c_void_p * len(devs))(*[d.ctx.value for d in devs])
+        out = (C.c_void_p * max(1, procs))()
+        check(_capi.lib().spg_partition(ctxs, len(devs), m.h, _SCHEMES.get(scheme, -1), procs, gpus_per_node, out))
+        r, c, _ = m.shape3
+        return [DeviceCsr(devs[t % len(devs)], out[t]) for t in range(procs)], make_tile_map(r, c, scheme, procs,
+                                                                                                 gpus_per_node)
+
+    def reassemble(self, tiles, tm: "TileMap") -> DeviceCsr:
+        """Device tile store: partition.cpp:224-261 on the GPU (spg_reassemble);
+        tiles may live on any device, the result on this one."""
+        arr = (C.c_void_p * max(1, len(tiles)))(*[t.h.value for t in tiles])
+        return self._out(_capi.lib().spg_reassemble, arr, len(tiles), int(tm.nrows), int(tm.ncols),
+                         _SCHEMES.get(tm.scheme, -1), tm.procs, int(tm.gpus_per_node) if tm.scheme == "trident" else 1)
+
     def column_normalize(self, m: DeviceCsr) -> None:
         check(_capi.lib().spg_column_normalize(self.ctx, m.h))
 
@@ -450,6 +469,17 @@ class TileMap:
     tiles: np.ndarray  # (procs, 4): row_begin, row_end, col_begin, col_end
 
 
+_SCHEMES = {"trident": 0, "grid2d": 1, "summa": 1, "rows1d": 2, "oned": 2}
+
+
+def tile_rects(nrows: int, ncols: int, scheme: str, procs: int, gpus_per_node: int) -> np.ndarray:
+    """The rectangles of make_tile_map as computed by the C ABI (spg_tile_rects)."""
+    out = np.zeros((max(procs, 1), 4), I64)
+    check(_capi.lib().spg_tile_rects(nrows, ncols, _SCHEMES.get(scheme, -1), procs, gpus_per_node,
+                                     out.ctypes.data_as(C.POINTER(C.c_int64))))
+    return out[:procs]
+
+
 def make_tile_map(nrows: int, ncols: int, scheme: str, procs: int, gpus_per_node: int) -> TileMap:
     """partition.cpp:95-159."""
     if procs <= 0:
@@ -594,11 +624,18 @@ def _devices_for(procs: int):
     return [default_device(d) for d in range(min(n, procs))]
 
 
-def _run_driver(fn, a, b, procs, lam, tiles_a, tiles_b, cmap, rounds, topo) -> DriverResult:
+def _run_driver(fn, a, b, procs, lam, scheme, cmap, rounds, topo) -> DriverResult:
+    """Device tile store end to end: ONE upload of each global operand, the
+    tiles split on the GPUs (spg_partition), the driver, the C tiles merged on
+    device 0 (spg_reassemble) and ONE download of C."""
     devs = _devices_for(procs)
     nctx = len(devs)
-    da = [devs[r % nctx].upload(tiles_a[r]) for r in range(procs)]
-    db = [devs[r % nctx].upload(tiles_b[r]) for r in range(procs)]
+    plam = lam if scheme == "trident" else 1
+    ga = devs[0].upload(a)
+    gb = ga if b is a else devs[0].upload(b)
+    da, _ = devs[0].partition(ga, scheme, procs, plam, devices=devs)
+    db, _ = devs[0].partition(gb, scheme, procs, plam, devices=devs)
+    del ga, gb
     ctxs = (C.c_void_p * nctx)(*[d.ctx.value for d in devs])
     ha = (C.c_void_p * procs)(*[x.h.value for x in da])
     hb = (C.c_void_p * procs)(*[x.h.value for x in db])
@@ -607,7 +644,7 @@ def _run_driver(fn, a, b, procs, lam, tiles_a, tiles_b, cmap, rounds, topo) -> D
     tl = (C.c_double * (procs * rounds * 4))()
     check(fn(ctxs, nctx, ha, hb, procs, lam, topo.index_width, topo.value_width, hc, cells, tl))
     dc = [DeviceCsr(devs[r % nctx], hc[r]) for r in range(procs)]
-    c = reassemble([x.download() for x in dc], cmap)
+    c = devs[0].reassemble(dc, cmap).download()
     led = np.array([[x.messages, x.nnz, x.bytes] for x in cells], np.uint64).reshape(procs, 2, 2, 3)
     tla = np.ctypeslib.as_array(tl).reshape(procs, rounds, 4).copy()
     makespan = float((tla[:, :, 1:].sum(axis=(1, 2))).max()) * 1e-3
@@ -619,10 +656,8 @@ def trident_spgemm(a, b, grid: TridentGrid, topo: TopologySpec | None = None) ->
     if int(a.ncols) != int(b.nrows):
         raise SpgError(2, f"trident_spgemm: a.ncols={a.ncols} != b.nrows={b.nrows}")
     topo = topo or TopologySpec(grid.gpus_per_node)
-    ta, _ = partition(a, "trident", grid.procs, grid.gpus_per_node)
-    tb, _ = partition(b, "trident", grid.procs, grid.gpus_per_node)
     cmap = make_tile_map(int(a.nrows), int(b.ncols), "trident", grid.procs, grid.gpus_per_node)
-    return _run_driver(_capi.lib().spg_trident_spgemm, a, b, grid.procs, grid.gpus_per_node, ta, tb, cmap, grid.q,
+    return _run_driver(_capi.lib().spg_trident_spgemm, a, b, grid.procs, grid.gpus_per_node, "trident", cmap, grid.q,
                        topo)
 
 
@@ -634,10 +669,8 @@ def summa_spgemm(a, b, procs: int, gpus_per_node: int, topo: TopologySpec | None
     if pr < 0:
         raise SpgError(4, f"summa: P={procs} is not a perfect square")
     topo = topo or TopologySpec(gpus_per_node)
-    ta, _ = partition(a, "grid2d", procs, 1)
-    tb, _ = partition(b, "grid2d", procs, 1)
     cmap = make_tile_map(int(a.nrows), int(b.ncols), "grid2d", procs, 1)
-    return _run_driver(_capi.lib().spg_summa_spgemm, a, b, procs, gpus_per_node, ta, tb, cmap, pr, topo)
+    return _run_driver(_capi.lib().spg_summa_spgemm, a, b, procs, gpus_per_node, "grid2d", cmap, pr, topo)
 
 
 def run_algo(algo: str, a, b, procs: int, gpus_per_node: int, topo: TopologySpec | None = None) -> DriverResult:

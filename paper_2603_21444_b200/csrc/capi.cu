@@ -423,6 +423,42 @@ spg_status spg_csr_copy(spg_ctx* ctx, const spg_csr* m, spg_csr** out) {
     });
 }
 
+spg_status spg_tile_rects(int64_t nrows, int64_t ncols, int scheme, int procs, int gpus_per_node,
+                          int64_t* rects_out) {
+    return guard([&] {
+        need(rects_out, "rects_out");
+        const auto r = tile_rects(nrows, ncols, scheme, procs, gpus_per_node);
+        for (size_t t = 0; t < r.size(); ++t) {
+            rects_out[4 * t + 0] = r[t].r0;
+            rects_out[4 * t + 1] = r[t].r1;
+            rects_out[4 * t + 2] = r[t].c0;
+            rects_out[4 * t + 3] = r[t].c1;
+        }
+    });
+}
+
+spg_status spg_partition(spg_ctx* const* ctxs, int nctx, const spg_csr* m, int scheme, int procs, int gpus_per_node,
+                         spg_csr** tiles_out) {
+    return guard([&] {
+        need(ctxs, "ctxs");
+        need(m, "m");
+        need(tiles_out, "tiles_out");
+        for (int i = 0; i < nctx; ++i) need(ctxs[i], "ctxs[i]");
+        partition_device(ctxs, nctx, m, scheme, procs, gpus_per_node, tiles_out);
+    });
+}
+
+spg_status spg_reassemble(spg_ctx* ctx, const spg_csr* const* tiles, int ntiles, int64_t nrows, int64_t ncols,
+                          int scheme, int procs, int gpus_per_node, spg_csr** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(out, "out");
+        if (ntiles > 0) need(tiles, "tiles");
+        DeviceScope ds(ctx->device);
+        *out = reassemble_device(ctx, tiles, ntiles, nrows, ncols, scheme, procs, gpus_per_node);
+    });
+}
+
 spg_status spg_spgemm_host(spg_ctx* ctx, int64_t a_nrows, int64_t a_ncols, const int64_t* a_rowptr,
                            const void* a_colind, const double* a_values, int64_t b_nrows, int64_t b_ncols,
                            const int64_t* b_rowptr, const void* b_colind, const double* b_values, int colind_width,

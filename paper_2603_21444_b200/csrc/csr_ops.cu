@@ -220,15 +220,18 @@ __global__ void k_extract_count(const int64_t* __restrict__ rp, const int32_t* _
     }
 }
 
+// G lanes per row (G = 8 for short rows: a 16-entry ER row split over q tiles
+// would leave most of a warp idle)
+template <int G>
 __global__ void k_extract_copy(const int64_t* __restrict__ beg, const int64_t* __restrict__ orp, int64_t rows,
                                const int32_t* __restrict__ col, const double* __restrict__ val, int64_t c0,
                                int32_t* __restrict__ ocol, double* __restrict__ oval) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
-    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t i = warp; i < rows; i += nwarps) {
+    const int lane = threadIdx.x & (G - 1);
+    const int64_t grp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) / G;
+    const int64_t ngrp = (int64_t(gridDim.x) * blockDim.x) / G;
+    for (int64_t i = grp; i < rows; i += ngrp) {
         const int64_t s = beg[i], o = orp[i], n = orp[i + 1] - o;
-        for (int64_t t = lane; t < n; t += 32) {
+        for (int64_t t = lane; t < n; t += G) {
             ocol[o + t] = static_cast<int32_t>(col[s + t] - c0);
             oval[o + t] = val[s + t];
         }
@@ -616,8 +619,12 @@ spg_csr* extract(spg_ctx* ctx, const spg_csr* m, int64_t r0, int64_t r1, int64_t
     exclusive_scan_i64(ctx, cnt, t->rowptr, rows);
     t->nnz = read_scalar(ctx, t->rowptr + rows);
     alloc_c_arrays(ctx, t, t->nnz);
-    k_extract_copy<<<grid_for(ctx, rows * 32), 256, 0, ctx->stream>>>(beg, t->rowptr, rows, m->colind, m->values, c0,
-                                                                      t->colind, t->values);
+    if (t->nnz <= 24 * rows)
+        k_extract_copy<8><<<grid_for(ctx, rows * 8), 256, 0, ctx->stream>>>(beg, t->rowptr, rows, m->colind, m->values,
+                                                                            c0, t->colind, t->values);
+    else
+        k_extract_copy<32><<<grid_for(ctx, rows * 32), 256, 0, ctx->stream>>>(beg, t->rowptr, rows, m->colind,
+                                                                              m->values, c0, t->colind, t->values);
     SPG_LAUNCH_CHECK();
     return t;
 }

@@ -185,6 +185,18 @@ spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n, cudaEvent_t 
 spg_csr* hconcat(spg_ctx* ctx, const spg_csr* const* parts, int n);
 spg_csr* extract(spg_ctx* ctx, const spg_csr* m, int64_t r0, int64_t r1, int64_t c0, int64_t c1);
 spg_csr* copy_csr(spg_ctx* ctx, const spg_csr* m);
+
+// Device tile store (tiles.cu): make_tile_map rectangles (partition.cpp:95-159),
+// partition (:161-222) onto the tiles' devices, reassemble (:224-261).
+// scheme: 0 trident, 1 grid2d, 2 rows1d (partition.hpp:10).
+struct TileRect {
+    int64_t r0, r1, c0, c1;
+};
+std::vector<TileRect> tile_rects(int64_t nrows, int64_t ncols, int scheme, int procs, int gpus_per_node);
+void partition_device(spg_ctx* const* ctxs, int nctx, const spg_csr* m, int scheme, int procs, int gpus_per_node,
+                      spg_csr** out);
+spg_csr* reassemble_device(spg_ctx* ctx, const spg_csr* const* tiles, int ntiles, int64_t nrows, int64_t ncols,
+                           int scheme, int procs, int gpus_per_node);
 void column_normalize(spg_ctx* ctx, spg_csr* m);
 spg_csr* prune(spg_ctx* ctx, const spg_csr* m, double threshold);
 void check_canonical(spg_ctx* ctx, const spg_csr* m);

@@ -1,7 +1,8 @@
 // Distributed drivers of the drop-in library (reference algorithms.cpp:24-174):
-// partition on the host, tiles uploaded to the GPUs of this box (rank r ->
-// device r % ndev), the exchange + multiply + merge run by the C ABI
-// (spg_trident_spgemm / spg_summa_spgemm), C tiles downloaded and reassembled.
+// each global operand uploaded once and split into tiles on the GPUs of this
+// box (spg_partition; rank r -> device r % ndev), the exchange + multiply +
+// merge run by the C ABI (spg_trident_spgemm / spg_summa_spgemm), C tiles
+// merged on device 0 (spg_reassemble) and downloaded once.
 #include "spgsim/algorithms.hpp"
 
 #include <algorithm>
@@ -27,20 +28,31 @@ namespace {
 using Driver = spg_status (*)(spg_ctx* const*, int, const spg_csr* const*, const spg_csr* const*, int, int, int, int,
                               spg_csr**, spg_ledger_cell*, double*);
 
-DriverResult run_device(Driver drv, const PartitionResult& pa, const PartitionResult& pb, const TileMap& cmap,
+DriverResult run_device(Driver drv, const CsrMatrix& a, const CsrMatrix& b, Scheme scheme, const TileMap& cmap,
                         int procs, int gpus_per_node, const TopologySpec& topo, int rounds) {
     const int ndev = detail::device_count();
     const int nctx = std::min(ndev, procs);
     std::vector<spg_ctx*> ctxs(static_cast<std::size_t>(nctx));
     for (int d = 0; d < nctx; ++d) ctxs[static_cast<std::size_t>(d)] = detail::context(d);
+    // Device tile store: one upload per global operand, tiles split on the GPUs
+    // (spg_partition, rank r on device r % ndev).
+    const int plam = scheme == Scheme::trident ? gpus_per_node : 1;
     std::vector<DevCsr> da, db;
     std::vector<const spg_csr*> ha, hb;
-    for (int r = 0; r < procs; ++r) {
-        spg_ctx* c = ctxs[static_cast<std::size_t>(r % nctx)];
-        da.push_back(detail::upload(c, pa.tiles[static_cast<std::size_t>(r)]));
-        db.push_back(detail::upload(c, pb.tiles[static_cast<std::size_t>(r)]));
-        ha.push_back(da.back().p);
-        hb.push_back(db.back().p);
+    auto split = [&](const CsrMatrix& g, std::vector<DevCsr>& own, std::vector<const spg_csr*>& view) {
+        DevCsr dg = detail::upload(ctxs[0], g);
+        std::vector<spg_csr*> t(static_cast<std::size_t>(procs), nullptr);
+        check(spg_partition(ctxs.data(), nctx, dg.p, static_cast<int>(scheme), procs, plam, t.data()));
+        for (auto* h : t) {
+            own.emplace_back(h);
+            view.push_back(h);
+        }
+    };
+    split(a, da, ha);
+    if (&a == &b) {
+        hb = ha;
+    } else {
+        split(b, db, hb);
     }
     std::vector<spg_csr*> hc(static_cast<std::size_t>(procs), nullptr);
     std::vector<spg_ledger_cell> cells(static_cast<std::size_t>(procs) * 4);
@@ -52,9 +64,15 @@ DriverResult run_device(Driver drv, const PartitionResult& pa, const PartitionRe
 
     DriverResult out;
     out.rounds = rounds;
-    std::vector<CsrMatrix> ctiles;
-    for (int r = 0; r < procs; ++r) ctiles.push_back(detail::download(ctxs[static_cast<std::size_t>(r % nctx)], dc[static_cast<std::size_t>(r)].p));
-    out.c = reassemble(ctiles, cmap);
+    {  // C tiles merged on device 0 (spg_reassemble), one download
+        std::vector<const spg_csr*> hv;
+        for (auto& d : dc) hv.push_back(d.p);
+        spg_csr* g = nullptr;
+        check(spg_reassemble(ctxs[0], hv.data(), procs, cmap.nrows, cmap.ncols, static_cast<int>(cmap.scheme), procs,
+                             plam, &g));
+        DevCsr dg(g);
+        out.c = detail::download(ctxs[0], dg.p);
+    }
     std::vector<int> nodes(static_cast<std::size_t>(procs));
     for (int r = 0; r < procs; ++r) nodes[static_cast<std::size_t>(r)] = r / gpus_per_node;
     out.ledger = CommLedger(procs, nodes);
@@ -96,22 +114,18 @@ DriverResult trident_spgemm(const CsrMatrix& a, const CsrMatrix& b, const Triden
         throw DimensionError("trident_spgemm: a.ncols=" + std::to_string(a.ncols) + " != b.nrows=" + std::to_string(b.nrows));
     topo.validate();
     const int P = grid.procs, lam = grid.gpus_per_node;
-    const PartitionResult pa = partition(a, Scheme::trident, P, lam);
-    const PartitionResult pb = partition(b, Scheme::trident, P, lam);
     const TileMap cmap = make_tile_map(a.nrows, b.ncols, Scheme::trident, P, lam);
-    return run_device(spg_trident_spgemm, pa, pb, cmap, P, lam, topo, grid.q);
+    return run_device(spg_trident_spgemm, a, b, Scheme::trident, cmap, P, lam, topo, grid.q);
 }
 
 DriverResult summa_spgemm(const CsrMatrix& a, const CsrMatrix& b, int procs, int gpus_per_node, const TopologySpec& topo) {
     if (a.ncols != b.nrows)
         throw DimensionError("summa_spgemm: a.ncols=" + std::to_string(a.ncols) + " != b.nrows=" + std::to_string(b.nrows));
     topo.validate();
-    const PartitionResult pa = partition(a, Scheme::grid2d, procs, 1);  // GridError when P is not a square
-    const PartitionResult pb = partition(b, Scheme::grid2d, procs, 1);
-    const TileMap cmap = make_tile_map(a.nrows, b.ncols, Scheme::grid2d, procs, 1);
+    const TileMap cmap = make_tile_map(a.nrows, b.ncols, Scheme::grid2d, procs, 1);  // GridError when P is not a square
     int pr = 0;
     while ((pr + 1) * (pr + 1) <= procs) ++pr;
-    return run_device(spg_summa_spgemm, pa, pb, cmap, procs, gpus_per_node, topo, pr);
+    return run_device(spg_summa_spgemm, a, b, Scheme::grid2d, cmap, procs, gpus_per_node, topo, pr);
 }
 
 DriverResult run_algo(Algo algo, const CsrMatrix& a, const CsrMatrix& b, int procs, int gpus_per_node,

@@ -114,3 +114,28 @@ def test_csr_canonical_checker():
     m = spg.CsrMatrix(2, 2, np.array([0, 1, 1]), np.array([5]), np.ones(1))
     assert not m.is_canonical()
     assert spg.gen_erdos_renyi(50, 0.2, 1).is_canonical()
+
+
+@pytest.mark.parametrize("P,lam", grids())
+def test_capi_tile_rects_match_reference(P, lam):
+    # spg_tile_rects (the C ABI's make_tile_map, used by the device tile store)
+    a = csr("er300_p3_A")
+    assert np.array_equal(spg.tile_rects(int(a.nrows), int(a.ncols), "trident", P, lam), z()[f"part_P{P}_L{lam}_rects"])
+
+
+@pytest.mark.parametrize("shape", [(8, 8), (2, 5), (300, 7), (0, 4), (17, 1)])
+@pytest.mark.parametrize("scheme,P,lam", [("trident", 16, 4), ("trident", 8, 2), ("trident", 4, 1), ("grid2d", 9, 1),
+                                          ("grid2d", 4, 1), ("rows1d", 5, 1), ("rows1d", 1, 1)])
+def test_capi_tile_rects_match_make_tile_map(shape, scheme, P, lam):
+    tm = spg.make_tile_map(*shape, scheme, P, lam)
+    assert np.array_equal(spg.tile_rects(*shape, scheme, P, lam), tm.tiles)
+
+
+def test_capi_tile_rects_grid_errors():
+    for args in [(4, 4, "grid2d", 8, 1), (4, 4, "trident", 6, 4), (4, 4, "trident", 8, 1), (4, 4, "rows1d", 0, 1)]:
+        with pytest.raises(spg.SpgError) as e:
+            spg.tile_rects(*args)
+        assert e.value.kind == "GridError"
+    with pytest.raises(spg.SpgError) as e:
+        spg.tile_rects(4, 4, "bogus", 4, 1)
+    assert e.value.kind == "ParameterError"
