@@ -156,6 +156,14 @@ spg_status spg_spgemm_host(spg_ctx* ctx, int64_t a_nrows, int64_t a_ncols, const
 /* MCL post-step on device (csr.cpp:224-249): column_normalize then prune. */
 spg_status spg_column_normalize(spg_ctx* ctx, spg_csr* m);
 spg_status spg_prune(spg_ctx* ctx, const spg_csr* m, double threshold, spg_csr** out);
+/* In-place v = pow(v, exponent) (csr.hpp:80 elementwise_power, csr.cpp:251-255);
+ * exponent 2 is the correctly rounded square. */
+spg_status spg_elementwise_power(spg_ctx* ctx, spg_csr* m, double exponent);
+/* The MCL iteration post-step after the expansion (apps.cpp:79-82):
+ * *out = column_normalize(elementwise_power(prune(column_normalize(c), prune_threshold), inflation)).
+ * The first normalize, the prune and the power are one fused pass over c
+ * (c is not modified); SPG_PARAMETER_ERROR on a negative threshold. */
+spg_status spg_mcl_poststep(spg_ctx* ctx, const spg_csr* c, double prune_threshold, double inflation, spg_csr** out);
 
 /* --------------------------------------------------- distributed drivers */
 /* Ledger cell, mirrors LedgerCell (netmodel.hpp:53-63). */

@@ -21,6 +21,8 @@ import ctypes as C
 import os
 from dataclasses import dataclass
 
+import math
+
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -82,6 +84,7 @@ def _R():
         lib.ref_permute_random.argtypes = [vp, u64, C.POINTER(vp)]
         lib.ref_column_normalize.argtypes = [vp, C.POINTER(vp)]
         lib.ref_prune.argtypes = [vp, f64, C.POINTER(vp)]
+        lib.ref_elementwise_power.argtypes = [vp, f64, C.POINTER(vp)]
         lib.ref_spgemm_local.argtypes = [vp, vp, C.POINTER(vp)]
         lib.ref_spgemm_local_timed.argtypes = [vp, vp, C.POINTER(f64), C.POINTER(i64), C.POINTER(vp)]
         lib.ref_spgeam.argtypes = [vp, vp, C.POINTER(vp)]
@@ -167,6 +170,21 @@ def ref_permute_random(m, seed: int, handle: bool = False):
     hm = _h(m)
     h = _out(_R().ref_permute_random, hm.ptr, seed)
     return h if handle else h.to_csr()
+
+
+def ref_elementwise_power(m, r: float, handle: bool = False):
+    """csr.cpp:251-255 (the reference itself)."""
+    hm = _h(m)
+    h = _out(_R().ref_elementwise_power, hm.ptr, float(r))
+    return h if handle else h.to_csr()
+
+
+def ref_mcl_poststep(c, theta: float, r: float) -> Csr:
+    """apps.cpp:79-82 with the reference's own functions."""
+    m = ref_column_normalize(c, handle=True)
+    m = ref_prune(m, theta, handle=True)
+    m = ref_elementwise_power(m, r, handle=True)
+    return ref_column_normalize(m)
 
 
 def ref_column_normalize(m, handle: bool = False):
@@ -376,6 +394,21 @@ def port_column_normalize(m) -> Csr:
     o = _to_o(c)
     _P().oracle_column_normalize(C.byref(o))
     return c
+
+
+def port_elementwise_power(m, r: float) -> Csr:
+    """csr.cpp:251-255: v = std::pow(v, r) per stored value. math.pow is the
+    host libm's pow, bit-identical to the reference's (numpy's own power is
+    not, and neither is the correctly rounded v*v for r = 2: glibc's pow is
+    within ~0.52 ulp, not correctly rounded)."""
+    v = np.array(m.values, np.float64)
+    out = np.fromiter((math.pow(x, r) for x in v), np.float64, count=v.size)
+    return Csr(m.nrows, m.ncols, np.array(m.rowptr, np.int64), np.array(m.colind, np.int64), out)
+
+
+def port_mcl_poststep(c, theta: float, r: float) -> Csr:
+    """apps.cpp:79-82 composed from the port's own steps."""
+    return port_column_normalize(port_elementwise_power(port_prune(port_column_normalize(c), theta), r))
 
 
 def port_prune(m, theta: float) -> Csr:

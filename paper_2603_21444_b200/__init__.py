@@ -21,7 +21,7 @@ from ._capi import SpgError, check
 
 __all__ = [
     "CsrMatrix", "Device", "DeviceCsr", "SpgError", "spgemm_local", "spgeam", "vconcat", "column_normalize",
-    "prune", "pattern_equal", "allclose", "gen_erdos_renyi", "gen_erdos_renyi_rect", "gen_rmat", "transpose",
+    "prune", "elementwise_power", "mcl_poststep", "pattern_equal", "allclose", "gen_erdos_renyi", "gen_erdos_renyi_rect", "gen_rmat", "transpose",
     "TridentGrid", "TopologySpec", "block_bounds", "make_tile_map", "partition", "reassemble", "trident_spgemm",
     "summa_spgemm", "run_algo", "DriverResult", "trident_ledger", "payload_bytes", "default_device",
 ]
@@ -249,6 +249,13 @@ class Device:
     def prune(self, m: DeviceCsr, theta: float) -> DeviceCsr:
         return self._out(_capi.lib().spg_prune, m.h, float(theta))
 
+    def elementwise_power(self, m: DeviceCsr, exponent: float) -> None:
+        check(_capi.lib().spg_elementwise_power(self.ctx, m.h, float(exponent)))
+
+    def mcl_poststep(self, c: DeviceCsr, prune_threshold: float, inflation: float) -> DeviceCsr:
+        """apps.cpp:79-82: column_normalize(power(prune(column_normalize(c)))), fused."""
+        return self._out(_capi.lib().spg_mcl_poststep, c.h, float(prune_threshold), float(inflation))
+
     # kernel timing (CUDA events on the context stream)
     def timing(self, on: bool = True) -> None:
         check(_capi.lib().spg_timing_enable(self.ctx, 1 if on else 0))
@@ -312,6 +319,20 @@ def prune(a, threshold: float) -> CsrMatrix:
         raise SpgError(3, "prune: negative threshold")
     d = default_device()
     return d.prune(d.upload(a), threshold).download()
+
+
+def elementwise_power(a, exponent: float) -> CsrMatrix:
+    """csr.cpp:251-255."""
+    d = default_device()
+    m = d.upload(a)
+    d.elementwise_power(m, exponent)
+    return m.download()
+
+
+def mcl_poststep(c, prune_threshold: float = 0.002, inflation: float = 2.0) -> CsrMatrix:
+    """The post-step of one MCL iteration (apps.cpp:79-82) on the GPU."""
+    d = default_device()
+    return d.mcl_poststep(d.upload(c), prune_threshold, inflation).download()
 
 
 def vconcat(slices) -> CsrMatrix:

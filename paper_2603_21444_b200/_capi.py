@@ -19,7 +19,7 @@ EXPORTS = [
     "spg_ctx_device", "spg_timing_enable", "spg_timing_reset", "spg_timing_read", "spg_csr_upload",
     "spg_csr_zeros", "spg_csr_shape", "spg_csr_upload_into", "spg_csr_download", "spg_csr_check", "spg_csr_free",
     "spg_csr_device_ptrs", "spg_spgemm", "spg_spgemm_products", "spg_spgeam", "spg_spgeam_inplace",
-    "spg_vconcat", "spg_csr_extract", "spg_csr_copy", "spg_tile_rects", "spg_partition", "spg_reassemble", "spg_spgemm_host", "spg_column_normalize", "spg_prune",
+    "spg_vconcat", "spg_csr_extract", "spg_csr_copy", "spg_tile_rects", "spg_partition", "spg_reassemble", "spg_spgemm_host", "spg_column_normalize", "spg_prune", "spg_elementwise_power", "spg_mcl_poststep",
     "spg_trident_grid", "spg_trident_spgemm", "spg_summa_spgemm",
     "spg_host_register", "spg_host_unregister",
     "spg_csr_ipc_export", "spg_csr_ipc_open", "spg_csr_make_shareable", "spg_trident_rank",
@@ -83,6 +83,8 @@ def lib() -> C.CDLL:
         "spg_spgemm_host": (st, [vp, i64, i64, vp, vp, vp, i64, i64, vp, vp, vp, i32, P(vp)]),
         "spg_column_normalize": (st, [vp, vp]),
         "spg_prune": (st, [vp, vp, f64, P(vp)]),
+        "spg_elementwise_power": (st, [vp, vp, f64]),
+        "spg_mcl_poststep": (st, [vp, vp, f64, f64, P(vp)]),
         "spg_trident_grid": (st, [i32, i32, P(i32)]),
         "spg_trident_spgemm": (st, [P(vp), i32, P(vp), P(vp), i32, i32, i32, i32, P(vp), P(LedgerCell), P(f64)]),
         "spg_summa_spgemm": (st, [P(vp), i32, P(vp), P(vp), i32, i32, i32, i32, P(vp), P(LedgerCell), P(f64)]),

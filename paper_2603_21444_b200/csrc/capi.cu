@@ -495,6 +495,25 @@ spg_status spg_prune(spg_ctx* ctx, const spg_csr* m, double threshold, spg_csr**
     });
 }
 
+spg_status spg_elementwise_power(spg_ctx* ctx, spg_csr* m, double exponent) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(m, "m");
+        DeviceScope ds(ctx->device);
+        elementwise_power(ctx, m, exponent);
+    });
+}
+
+spg_status spg_mcl_poststep(spg_ctx* ctx, const spg_csr* c, double prune_threshold, double inflation, spg_csr** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(c, "c");
+        need(out, "out");
+        DeviceScope ds(ctx->device);
+        *out = mcl_poststep(ctx, c, prune_threshold, inflation);
+    });
+}
+
 spg_status spg_trident_grid(int procs, int gpus_per_node, int* q) {
     return guard([&] {
         need(q, "q");

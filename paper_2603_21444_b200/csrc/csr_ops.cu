@@ -264,23 +264,42 @@ __global__ void k_scale_cols(const int32_t* __restrict__ col, double* __restrict
 }
 
 // -------------------------------------------------------------------- prune
-__global__ void k_prune_count(const int64_t* __restrict__ rp, const double* __restrict__ val, int64_t m,
-                              double th, int64_t* __restrict__ cnt) {
+// MCL transform of a value before the prune test (apps.cpp:79-81): with
+// colsum, v' = v / colsum[col] when the sum is nonzero (column_normalize,
+// csr.cpp:228-232); the kept value is written as pow(v', r) (elementwise_power,
+// csr.cpp:251-255; r = 2 is the correctly rounded square, r = 1 the identity).
+__device__ __forceinline__ double mcl_scale(double v, int32_t c, const double* __restrict__ colsum) {
+    if (colsum) {
+        const double s = colsum[c];
+        if (s != 0.0) v = __ddiv_rn(v, s);
+    }
+    return v;
+}
+__device__ __forceinline__ double mcl_power(double v, double r) {
+    if (r == 1.0) return v;
+    if (r == 2.0) return __dmul_rn(v, v);
+    return pow(v, r);
+}
+
+__global__ void k_prune_count(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                              const double* __restrict__ val, int64_t m, double th, const double* __restrict__ colsum,
+                              int64_t* __restrict__ cnt) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
     for (int64_t i = warp; i < m; i += nwarps) {
         int64_t c = 0;
-        for (int64_t t = rp[i] + lane; t < rp[i + 1]; t += 32) c += !(val[t] < th);
+        for (int64_t t = rp[i] + lane; t < rp[i + 1]; t += 32)
+            c += !(mcl_scale(val[t], colsum ? col[t] : 0, colsum) < th);
 #pragma unroll
         for (int k = 16; k > 0; k >>= 1) c += __shfl_xor_sync(0xffffffffu, c, k);
         if (lane == 0) cnt[i] = c;
     }
 }
-
 __global__ void k_prune_copy(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                             const double* __restrict__ val, int64_t m, double th, const int64_t* __restrict__ orp,
-                             int32_t* __restrict__ ocol, double* __restrict__ oval) {
+                             const double* __restrict__ val, int64_t m, double th, const double* __restrict__ colsum,
+                             double r, const int64_t* __restrict__ orp, int32_t* __restrict__ ocol,
+                             double* __restrict__ oval) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -288,16 +307,26 @@ __global__ void k_prune_copy(const int64_t* __restrict__ rp, const int32_t* __re
         int64_t o = orp[i];
         for (int64_t base = rp[i]; base < rp[i + 1]; base += 32) {
             const int64_t t = base + lane;
-            const bool keep = t < rp[i + 1] && !(val[t] < th);
+            int32_t c = 0;
+            double v = 0.0;
+            if (t < rp[i + 1]) {
+                c = col[t];
+                v = mcl_scale(val[t], c, colsum);
+            }
+            const bool keep = t < rp[i + 1] && !(v < th);
             const unsigned mask = __ballot_sync(0xffffffffu, keep);
             if (keep) {
                 const int64_t w = o + __popc(mask & ((1u << lane) - 1));
-                ocol[w] = col[t];
-                oval[w] = val[t];
+                ocol[w] = c;
+                oval[w] = mcl_power(v, r);
             }
             o += __popc(mask);
         }
     }
+}
+
+__global__ void k_power(double* __restrict__ val, int64_t nnz, double r) {
+    GRID_STRIDE(t, nnz) val[t] = mcl_power(val[t], r);
 }
 
 // -------------------------------------------------------- canonical check
@@ -629,50 +658,95 @@ spg_csr* extract(spg_ctx* ctx, const spg_csr* m, int64_t r0, int64_t r1, int64_t
     return t;
 }
 
-void column_normalize(spg_ctx* ctx, spg_csr* m) {
+namespace {
+// Column sums in CSR storage order (csr.cpp:225-227) into colsum[ncols]:
+// stable radix sort of (column -> value) makes each column's values
+// contiguous in storage (row) order, then one thread per column sums them
+// sequentially like the reference loop.
+void column_sums(spg_ctx* ctx, const spg_csr* m, double* colsum) {
     const int64_t nnz = m->nnz;
+    SPG_CUDA(cudaMemsetAsync(colsum, 0, m->ncols * sizeof(double), ctx->stream));
     if (nnz == 0) return;
     if (nnz > INT32_MAX) fail(SPG_PARAMETER_ERROR, "column_normalize: nnz exceeds 2^31");
-    // stable radix sort of (column -> value): each column's values end up
-    // contiguous in storage (row) order, then one thread per column sums them
-    // sequentially like the reference loop (csr.cpp:225-227)
     DBuf<int32_t> keys(ctx, nnz);
     DBuf<double> vals(ctx, nnz);
-    DBuf<double> colsum(ctx, m->ncols);
-    KTime kt(ctx, "column_normalize");
     int bits = 1;
     while ((int64_t(1) << bits) < m->ncols) ++bits;
     size_t tmp = 0;
     SPG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, m->colind, keys.get(), m->values, vals.get(),
                                              static_cast<int>(nnz), 0, bits, ctx->stream));
     DBuf<unsigned char> t(ctx, tmp);
-    SPG_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, m->colind, keys.get(), m->values, vals.get(),
-                                             static_cast<int>(nnz), 0, bits, ctx->stream));
-    SPG_CUDA(cudaMemsetAsync(colsum.get(), 0, m->ncols * sizeof(double), ctx->stream));
+    {
+        KTime kt(ctx, "colsum_sort");
+        SPG_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, m->colind, keys.get(), m->values, vals.get(),
+                                                 static_cast<int>(nnz), 0, bits, ctx->stream));
+    }
+    KTime kt(ctx, "colsum_runs");
     k_colsum_runs<<<grid_for(ctx, nnz), 256, 0, ctx->stream>>>(keys, vals, nnz, colsum);
-    k_scale_cols<<<grid_for(ctx, nnz), 256, 0, ctx->stream>>>(m->colind, m->values, nnz, colsum);
+    SPG_LAUNCH_CHECK();
+}
+
+// Rows of a kept where !(v' < th), v' the MCL-scaled value; kept values raised to r.
+spg_csr* prune_transform(spg_ctx* ctx, const spg_csr* a, double th, const double* colsum, double r) {
+    const int64_t m = a->nrows;
+    DBuf<int64_t> cnt(ctx, m + 1);
+    spg_csr* out = new_csr(ctx, m, a->ncols, -1);
+    if (m) {
+        k_prune_count<<<grid_for(ctx, m * 32), 256, 0, ctx->stream>>>(a->rowptr, a->colind, a->values, m, th, colsum,
+                                                                      cnt);
+        SPG_LAUNCH_CHECK();
+    }
+    exclusive_scan_i64(ctx, cnt, out->rowptr, m);
+    out->nnz = read_scalar(ctx, out->rowptr + m);
+    alloc_c_arrays(ctx, out, out->nnz);
+    if (m && out->nnz) {
+        k_prune_copy<<<grid_for(ctx, m * 32), 256, 0, ctx->stream>>>(a->rowptr, a->colind, a->values, m, th, colsum, r,
+                                                                     out->rowptr, out->colind, out->values);
+        SPG_LAUNCH_CHECK();
+    }
+    return out;
+}
+}  // namespace
+
+void column_normalize(spg_ctx* ctx, spg_csr* m) {
+    if (m->nnz == 0) return;
+    DBuf<double> colsum(ctx, m->ncols);
+    KTime kt(ctx, "column_normalize");
+    column_sums(ctx, m, colsum);
+    k_scale_cols<<<grid_for(ctx, m->nnz), 256, 0, ctx->stream>>>(m->colind, m->values, m->nnz, colsum);
     SPG_LAUNCH_CHECK();
 }
 
 spg_csr* prune(spg_ctx* ctx, const spg_csr* a, double th) {
     if (th < 0.0) fail(SPG_PARAMETER_ERROR, "prune: negative threshold");
-    const int64_t m = a->nrows;
-    DBuf<int64_t> cnt(ctx, m + 1);
-    spg_csr* r = new_csr(ctx, m, a->ncols, -1);
     KTime kt(ctx, "prune");
-    if (m) {
-        k_prune_count<<<grid_for(ctx, m * 32), 256, 0, ctx->stream>>>(a->rowptr, a->values, m, th, cnt);
-        SPG_LAUNCH_CHECK();
+    return prune_transform(ctx, a, th, nullptr, 1.0);
+}
+
+void elementwise_power(spg_ctx* ctx, spg_csr* m, double r) {
+    if (m->nnz == 0 || r == 1.0) return;
+    KTime kt(ctx, "elementwise_power");
+    k_power<<<grid_for(ctx, m->nnz), 256, 0, ctx->stream>>>(m->values, m->nnz, r);
+    SPG_LAUNCH_CHECK();
+}
+
+spg_csr* mcl_poststep(spg_ctx* ctx, const spg_csr* c, double th, double r) {
+    if (th < 0.0) fail(SPG_PARAMETER_ERROR, "mcl: negative prune threshold");
+    spg_csr* out = nullptr;
+    {
+        // column_normalize + prune + elementwise_power in one pass over c
+        DBuf<double> colsum(ctx, c->ncols);
+        KTime kt(ctx, "mcl_normalize_prune_power");
+        column_sums(ctx, c, colsum);
+        out = prune_transform(ctx, c, th, colsum, r);
     }
-    exclusive_scan_i64(ctx, cnt, r->rowptr, m);
-    r->nnz = read_scalar(ctx, r->rowptr + m);
-    alloc_c_arrays(ctx, r, r->nnz);
-    if (m) {
-        k_prune_copy<<<grid_for(ctx, m * 32), 256, 0, ctx->stream>>>(a->rowptr, a->colind, a->values, m, th, r->rowptr,
-                                                                     r->colind, r->values);
-        SPG_LAUNCH_CHECK();
+    try {
+        column_normalize(ctx, out);
+    } catch (...) {
+        free_csr(out);
+        throw;
     }
-    return r;
+    return out;
 }
 
 void check_canonical(spg_ctx* ctx, const spg_csr* m) {

@@ -199,6 +199,9 @@ spg_csr* reassemble_device(spg_ctx* ctx, const spg_csr* const* tiles, int ntiles
                            int scheme, int procs, int gpus_per_node);
 void column_normalize(spg_ctx* ctx, spg_csr* m);
 spg_csr* prune(spg_ctx* ctx, const spg_csr* m, double threshold);
+void elementwise_power(spg_ctx* ctx, spg_csr* m, double exponent);
+// One MCL iteration's post-step (apps.cpp:79-82): column_normalize(power(prune(column_normalize(c))))
+spg_csr* mcl_poststep(spg_ctx* ctx, const spg_csr* c, double prune_threshold, double inflation);
 void check_canonical(spg_ctx* ctx, const spg_csr* m);
 
 // Exclusive scan of n int64 counts into out[0..n] (out[n] = total). In-place allowed.

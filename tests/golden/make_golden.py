@@ -5,6 +5,7 @@ oracle/Makefile). Run in the build container:  python tests/golden/make_golden.p
 small   : the reference's own known-answer cases (test_csr.cpp:24-109,182-200)
           plus small random products, spgeam, vconcat, partition tiles and
           trident/SUMMA ledgers  -> small.npz  (full arrays)
+mcl4    : adds one MCL post-step digest of config 4 to config4.json
 configs : digests of the benchmark configs' C = A*B (nnz, sha256 of rowptr /
           colind / values, sampled rows) -> config<k>.json
 """
@@ -159,6 +160,26 @@ def config(k):
     print(f"config{k}: nnz={d['nnz']} ref {secs:.1f}s")
 
 
+def mcl4():
+    """Adds to config4.json the digest of one MCL post-step of config 4's
+    product with the reference's own functions (apps.cpp:79-82: normalize,
+    prune 0.002, elementwise_power 2, normalize)."""
+    m = O.ref_gen_erdos_renyi(1 << 21, 16.0 / (1 << 21), 1, handle=True)
+    a = O.ref_column_normalize(m, handle=True)
+    _, _, c = O.ref_spgemm_local_timed(a, a, keep=True)
+    t0 = time.time()
+    s = O.ref_mcl_poststep(c, 0.002, 2.0)
+    secs = time.time() - t0
+    path = os.path.join(HERE, "config4.json")
+    with open(path) as f:
+        d = json.load(f)
+    d["mcl_step"] = {k2: v for k2, v in digest(s, secs, 64).items()}
+    d["mcl_step"]["params"] = {"prune_threshold": 0.002, "inflation": 2.0}
+    with open(path, "w") as f:
+        json.dump(d, f)
+    print(f"config4 mcl step: nnz={s.nnz} ref {secs:.1f}s")
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "small"
     if what in ("small", "all"):
@@ -166,5 +187,7 @@ if __name__ == "__main__":
     if what in ("configs", "all"):
         for k in (1, 4, 5, 2):
             config(k)
+    if what == "mcl4":
+        mcl4()
     if what.startswith("config") and what != "configs":
         config(int(what[6:]))

@@ -83,3 +83,15 @@ def test_reference_config1_products():
     assert O.port_products(a, a) == 1040687
     c = O.port_spgemm(a, a)
     assert c.nnz == 1038646
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("r", [2.0, 1.5, 1.0])
+def test_port_mcl_poststep_vs_reference(r):
+    # apps.cpp:79-82 post-step: the port against the reference's own functions
+    a = O.port_column_normalize(O.port_gen_erdos_renyi(400, 0.02, 11))
+    c = O.port_spgemm(a, a)
+    got, ref = O.port_mcl_poststep(c, 0.003, r), O.ref_mcl_poststep(c, 0.003, r)
+    assert O.pattern_equal(got, ref)
+    assert np.array_equal(got.values, ref.values)
+    assert np.array_equal(O.port_elementwise_power(c, r).values, O.ref_elementwise_power(c, r).values)
