@@ -243,15 +243,37 @@ __global__ void k_extract_copy(const int64_t* __restrict__ beg, const int64_t* _
 // stably radix-sorted by column (value as payload), then each column is summed
 // sequentially in storage order, so sums are bit-identical.
 
-__global__ void k_colsum_runs(const int32_t* __restrict__ keys, const double* __restrict__ sval, int64_t nnz,
-                              double* __restrict__ colsum) {
-    // one thread per run start (a run = one column, values in storage order)
-    GRID_STRIDE(t, nnz) {
-        if (t > 0 && keys[t - 1] == keys[t]) continue;
-        const int32_t c = keys[t];
-        double s = 0.0;
-        for (int64_t u = t; u < nnz && keys[u] == c; ++u) s = __dadd_rn(s, sval[u]);
-        colsum[c] = s;
+// Block per chunk of CS sorted entries, staged in smem with coalesced loads;
+// each run (column) whose head lies in the chunk is summed sequentially in
+// storage order by one thread (reading on into global memory when the run
+// crosses the chunk end). Run ends are found first so the dependent adds can
+// run over an unrolled, known-length loop.
+constexpr int CS_CHUNK = 2048;
+__global__ void __launch_bounds__(256) k_colsum_runs(const int32_t* __restrict__ keys, const double* __restrict__ sval,
+                                                     int64_t nnz, double* __restrict__ colsum) {
+    __shared__ int32_t sk[CS_CHUNK + 1];
+    __shared__ double sv[CS_CHUNK];
+    for (int64_t b = int64_t(blockIdx.x) * CS_CHUNK; b < nnz; b += int64_t(gridDim.x) * CS_CHUNK) {
+        const int n = static_cast<int>(nnz - b < CS_CHUNK ? nnz - b : CS_CHUNK);
+        for (int t = threadIdx.x; t < n; t += blockDim.x) {
+            sk[t + 1] = keys[b + t];
+            sv[t] = sval[b + t];
+        }
+        if (threadIdx.x == 0) sk[0] = b > 0 ? keys[b - 1] : -1;
+        __syncthreads();
+        for (int t = threadIdx.x; t < n; t += blockDim.x) {
+            const int32_t c = sk[t + 1];
+            if (sk[t] == c) continue;  // not a run head
+            int e = t + 1;
+            while (e < n && sk[e + 1] == c) ++e;
+            double acc = 0.0;
+#pragma unroll 8
+            for (int u = t; u < e; ++u) acc = __dadd_rn(acc, sv[u]);
+            if (e == n)  // the run goes on past the chunk
+                for (int64_t u = b + n; u < nnz && keys[u] == c; ++u) acc = __dadd_rn(acc, sval[u]);
+            colsum[c] = acc;
+        }
+        __syncthreads();
     }
 }
 
@@ -682,7 +704,8 @@ void column_sums(spg_ctx* ctx, const spg_csr* m, double* colsum) {
                                                  static_cast<int>(nnz), 0, bits, ctx->stream));
     }
     KTime kt(ctx, "colsum_runs");
-    k_colsum_runs<<<grid_for(ctx, nnz), 256, 0, ctx->stream>>>(keys, vals, nnz, colsum);
+    k_colsum_runs<<<static_cast<int>(std::min<int64_t>((nnz + CS_CHUNK - 1) / CS_CHUNK, int64_t(ctx->num_sms) * 8)), 256,
+                    0, ctx->stream>>>(keys, vals, nnz, colsum);
     SPG_LAUNCH_CHECK();
 }
 
