@@ -199,6 +199,17 @@ spg_status spg_summa_spgemm(spg_ctx* const* ctxs, int nctx, const spg_csr* const
                             int value_width, spg_csr** c_tiles_out, spg_ledger_cell* ledger_out,
                             double* timeline_out);
 
+/* Single-process sparsity-aware 1D driver (algorithms.cpp:176-269) on a
+ * rows1d partition of A and B (tile r on ctxs[r % nctx]). Rank p pulls exactly
+ * the B rows named by the distinct columns of its A block from their owners
+ * (read in place over NVLink), builds the reference's gathered K x n operand
+ * and multiplies. ledger_out as above (one request + one transfer per (rank,
+ * owner) with needed rows; node_of = rank / gpus_per_node); timeline_out: P*4
+ * doubles [exchange_ms, exposed_ms, multiply_ms, 0]. */
+spg_status spg_oned_spgemm(spg_ctx* const* ctxs, int nctx, const spg_csr* const* a_tiles,
+                           const spg_csr* const* b_tiles, int procs, int gpus_per_node, int index_width,
+                           int value_width, spg_csr** c_tiles_out, spg_ledger_cell* ledger_out,
+                           double* timeline_out);
 
 /* ------------------------------------------------------ host memory pinning */
 /* Page-lock caller host memory (cudaHostRegister) so uploads/downloads of that

@@ -23,7 +23,7 @@ __all__ = [
     "CsrMatrix", "Device", "DeviceCsr", "SpgError", "spgemm_local", "spgeam", "vconcat", "column_normalize",
     "prune", "elementwise_power", "mcl_poststep", "pattern_equal", "allclose", "gen_erdos_renyi", "gen_erdos_renyi_rect", "gen_rmat", "transpose",
     "TridentGrid", "TopologySpec", "block_bounds", "make_tile_map", "partition", "reassemble", "trident_spgemm",
-    "summa_spgemm", "run_algo", "DriverResult", "trident_ledger", "payload_bytes", "default_device",
+    "summa_spgemm", "oned_spgemm", "run_algo", "DriverResult", "trident_ledger", "payload_bytes", "default_device",
 ]
 
 I64 = np.int64
@@ -694,10 +694,23 @@ def summa_spgemm(a, b, procs: int, gpus_per_node: int, topo: TopologySpec | None
     return _run_driver(_capi.lib().spg_summa_spgemm, a, b, procs, gpus_per_node, "grid2d", cmap, pr, topo)
 
 
+def oned_spgemm(a, b, procs: int, gpus_per_node: int, topo: TopologySpec | None = None) -> DriverResult:
+    """algorithms.cpp:176-269: sparsity-aware 1D (row-selective B fetch)."""
+    if int(a.ncols) != int(b.nrows):
+        raise SpgError(2, f"oned_spgemm: a.ncols={a.ncols} != b.nrows={b.nrows}")
+    if procs <= 0:
+        raise SpgError(4, "oned: P must be positive")
+    topo = topo or TopologySpec(gpus_per_node)
+    cmap = make_tile_map(int(a.nrows), int(b.ncols), "rows1d", procs, 1)
+    return _run_driver(_capi.lib().spg_oned_spgemm, a, b, procs, gpus_per_node, "rows1d", cmap, 1, topo)
+
+
 def run_algo(algo: str, a, b, procs: int, gpus_per_node: int, topo: TopologySpec | None = None) -> DriverResult:
-    """algorithms.cpp:271-280 (the 1D driver is outside the hot path)."""
+    """algorithms.cpp:271-280."""
     if algo == "trident":
         return trident_spgemm(a, b, TridentGrid.create(procs, gpus_per_node), topo)
     if algo == "summa":
         return summa_spgemm(a, b, procs, gpus_per_node, topo)
-    raise SpgError(3, f"run_algo: '{algo}' is outside the B200 hot path")
+    if algo == "oned":
+        return oned_spgemm(a, b, procs, gpus_per_node, topo)
+    raise SpgError(3, f"run_algo: unknown algorithm '{algo}'")

@@ -20,7 +20,7 @@ EXPORTS = [
     "spg_csr_zeros", "spg_csr_shape", "spg_csr_upload_into", "spg_csr_download", "spg_csr_check", "spg_csr_free",
     "spg_csr_device_ptrs", "spg_spgemm", "spg_spgemm_products", "spg_spgeam", "spg_spgeam_inplace",
     "spg_vconcat", "spg_csr_extract", "spg_csr_copy", "spg_tile_rects", "spg_partition", "spg_reassemble", "spg_spgemm_host", "spg_column_normalize", "spg_prune", "spg_elementwise_power", "spg_mcl_poststep",
-    "spg_trident_grid", "spg_trident_spgemm", "spg_summa_spgemm",
+    "spg_trident_grid", "spg_trident_spgemm", "spg_summa_spgemm", "spg_oned_spgemm",
     "spg_host_register", "spg_host_unregister",
     "spg_csr_ipc_export", "spg_csr_ipc_open", "spg_csr_make_shareable", "spg_trident_rank",
 ]
@@ -87,6 +87,7 @@ def lib() -> C.CDLL:
         "spg_mcl_poststep": (st, [vp, vp, f64, f64, P(vp)]),
         "spg_trident_grid": (st, [i32, i32, P(i32)]),
         "spg_trident_spgemm": (st, [P(vp), i32, P(vp), P(vp), i32, i32, i32, i32, P(vp), P(LedgerCell), P(f64)]),
+        "spg_oned_spgemm": (st, [P(vp), i32, P(vp), P(vp), i32, i32, i32, i32, P(vp), P(LedgerCell), P(f64)]),
         "spg_summa_spgemm": (st, [P(vp), i32, P(vp), P(vp), i32, i32, i32, i32, P(vp), P(LedgerCell), P(f64)]),
         "spg_host_register": (st, [vp, C.c_size_t]),
         "spg_host_unregister": (st, [vp]),

@@ -128,14 +128,23 @@ DriverResult summa_spgemm(const CsrMatrix& a, const CsrMatrix& b, int procs, int
     return run_device(spg_summa_spgemm, a, b, Scheme::grid2d, cmap, procs, gpus_per_node, topo, pr);
 }
 
+DriverResult oned_spgemm(const CsrMatrix& a, const CsrMatrix& b, int procs, int gpus_per_node, const TopologySpec& topo) {
+    if (a.ncols != b.nrows)
+        throw DimensionError("oned_spgemm: a.ncols=" + std::to_string(a.ncols) + " != b.nrows=" + std::to_string(b.nrows));
+    if (procs <= 0) throw GridError("oned: P must be positive");
+    topo.validate();
+    const TileMap cmap = make_tile_map(a.nrows, b.ncols, Scheme::rows1d, procs, 1);
+    return run_device(spg_oned_spgemm, a, b, Scheme::rows1d, cmap, procs, gpus_per_node, topo, 1);
+}
+
 DriverResult run_algo(Algo algo, const CsrMatrix& a, const CsrMatrix& b, int procs, int gpus_per_node,
                       const TopologySpec& topo) {
     switch (algo) {
         case Algo::trident: return trident_spgemm(a, b, TridentGrid::create(procs, gpus_per_node), topo);
         case Algo::summa: return summa_spgemm(a, b, procs, gpus_per_node, topo);
-        case Algo::oned: break;
+        case Algo::oned: return oned_spgemm(a, b, procs, gpus_per_node, topo);
     }
-    throw ParameterError("run_algo: the 1D driver is outside the B200 hot path");
+    throw ParameterError("run_algo: bad algorithm");
 }
 
 }  // namespace spgsim

@@ -172,6 +172,12 @@ TEST_CASE("trident and SUMMA reproduce the serial product") {
         const DriverResult r = summa_spgemm(a, b, P, 2, TopologySpec::preset(0, 2));
         CHECK(allclose(r.c, ref, 1e-12));
     }
+    for (int P : {1, 3, 4}) {  // sparsity-aware 1D (algorithms.cpp:176-269): same k order, bit-identical
+        const DriverResult r = run_algo(Algo::oned, a, b, P, 2, TopologySpec::preset(0, 2));
+        CHECK(r.c == ref);
+        CHECK(r.rounds == 1);
+    }
+    CHECK_THROWS_AS(oned_spgemm(a, b, 0, 2, TopologySpec::preset()), GridError);
     CHECK_THROWS_AS(trident_spgemm(a, b, TridentGrid::create(12, 4), TopologySpec::preset()), GridError);
     CHECK_THROWS_AS(summa_spgemm(a, b, 8, 2, TopologySpec::preset()), GridError);
     // rectangular: A (300x200) * A^T
