@@ -96,6 +96,10 @@ spg_status spg_csr_download(spg_ctx* ctx, const spg_csr* m, int64_t* rowptr, voi
 /* Device-side canonical check (csr.cpp:30-50): SPG_OK or SPG_ERROR with a
  * message naming the first violated invariant. */
 spg_status spg_csr_check(spg_ctx* ctx, const spg_csr* m);
+/* result_checksum (report.cpp:11-26) computed on the device: nnz and the
+ * order-independent 64-bit hash of (row, col, llround(v*1e9)) — identical to
+ * the reference's, so a C that never leaves HBM can be compared with it. */
+spg_status spg_result_checksum(spg_ctx* ctx, const spg_csr* m, int64_t* nnz, uint64_t* hash);
 spg_status spg_csr_free(spg_csr* m);
 /* Raw device pointers of a handle (rowptr int64*, colind int32*, values double*). */
 spg_status spg_csr_device_ptrs(const spg_csr* m, void** rowptr, void** colind, void** values);

@@ -85,6 +85,7 @@ def _R():
         lib.ref_column_normalize.argtypes = [vp, C.POINTER(vp)]
         lib.ref_prune.argtypes = [vp, f64, C.POINTER(vp)]
         lib.ref_elementwise_power.argtypes = [vp, f64, C.POINTER(vp)]
+        lib.ref_result_checksum.argtypes = [vp, C.POINTER(i64), C.POINTER(C.c_uint64)]
         lib.ref_spgemm_local.argtypes = [vp, vp, C.POINTER(vp)]
         lib.ref_spgemm_local_timed.argtypes = [vp, vp, C.POINTER(f64), C.POINTER(i64), C.POINTER(vp)]
         lib.ref_spgeam.argtypes = [vp, vp, C.POINTER(vp)]
@@ -177,6 +178,37 @@ def ref_elementwise_power(m, r: float, handle: bool = False):
     hm = _h(m)
     h = _out(_R().ref_elementwise_power, hm.ptr, float(r))
     return h if handle else h.to_csr()
+
+
+def ref_result_checksum(m):
+    """report.cpp:11-26 (the reference itself) -> (nnz, hash)."""
+    hm = _h(m)
+    n, h = C.c_int64(), C.c_uint64()
+    _chk(_R().ref_result_checksum(hm.ptr, C.byref(n), C.byref(h)))
+    return n.value, h.value
+
+
+def port_result_checksum(m):
+    """report.cpp:11-26 restated in numpy: sum over entries (mod 2^64) of
+    mix64(mix64(mix64(row + K) ^ col) ^ llround(v * 1e9))."""
+    M1, M2 = np.uint64(0xBF58476D1CE4E5B9), np.uint64(0x94D049BB133111EB)
+
+    def mix64(x):
+        x = (x ^ (x >> np.uint64(30))) * M1
+        x = (x ^ (x >> np.uint64(27))) * M2
+        return x ^ (x >> np.uint64(31))
+
+    rp = np.asarray(m.rowptr, np.int64)
+    rows = np.repeat(np.arange(int(m.nrows), dtype=np.uint64), np.diff(rp))
+    v = np.asarray(m.values, np.float64) * 1e9
+    q = np.where(v >= 0, np.floor(v + 0.5), np.ceil(v - 0.5))  # llround: halves away from zero
+    # (v + 0.5 is exact for |v| < 2^52; beyond that v is already an integer)
+    q = np.where(np.abs(v) >= 2.0 ** 52, v, q).astype(np.int64).view(np.uint64)
+    with np.errstate(over="ignore"):
+        h = mix64(rows + np.uint64(0x51ED270B9A3E51EB))
+        h = mix64(h ^ np.asarray(m.colind, np.int64).view(np.uint64))
+        h = mix64(h ^ q)
+        return int(rp[-1]), int(np.sum(h, dtype=np.uint64))
 
 
 def ref_mcl_poststep(c, theta: float, r: float) -> Csr:

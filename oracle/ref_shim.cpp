@@ -14,7 +14,7 @@
 //   ref_from_triplets    -> csr.cpp:61-88         (from_triplets)
 //   ref_permute_random   -> csr.cpp:104-112, 198-222
 //   ref_column_normalize -> csr.cpp:224-234 ; ref_prune -> csr.cpp:236-249
-//   ref_elementwise_power -> csr.cpp:251-255
+//   ref_elementwise_power -> csr.cpp:251-255 ; ref_result_checksum -> report.cpp:11-26
 //   ref_partition        -> partition.cpp:161-222 ; ref_reassemble -> :224-261
 //   ref_trident          -> algorithms.cpp:24-101 (trident_spgemm)
 //   ref_summa            -> algorithms.cpp:103-174 (summa_spgemm)
@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "spgsim/algorithms.hpp"
+#include "spgsim/report.hpp"
 #include "spgsim/csr.hpp"
 #include "spgsim/netmodel.hpp"
 #include "spgsim/partition.hpp"
@@ -135,6 +136,14 @@ int ref_permute_random(const void* a, std::uint64_t seed, void** out) {
 
 int ref_column_normalize(const void* a, void** out) {
     return guarded([&] { *out = box(column_normalize(*static_cast<const CsrMatrix*>(a))); });
+}
+
+int ref_result_checksum(const void* a, std::int64_t* nnz, std::uint64_t* hash) {
+    return guarded([&] {
+        const auto cs = result_checksum(*static_cast<const CsrMatrix*>(a));
+        *nnz = cs.nnz;
+        *hash = cs.hash;
+    });
 }
 
 int ref_elementwise_power(const void* a, double r, void** out) {

@@ -23,7 +23,7 @@ __all__ = [
     "CsrMatrix", "Device", "DeviceCsr", "SpgError", "spgemm_local", "spgeam", "vconcat", "column_normalize",
     "prune", "elementwise_power", "mcl_poststep", "pattern_equal", "allclose", "gen_erdos_renyi", "gen_erdos_renyi_rect", "gen_rmat", "transpose",
     "TridentGrid", "TopologySpec", "block_bounds", "make_tile_map", "partition", "reassemble", "trident_spgemm",
-    "summa_spgemm", "oned_spgemm", "run_algo", "DriverResult", "trident_ledger", "payload_bytes", "default_device",
+    "summa_spgemm", "oned_spgemm", "run_algo", "DriverResult", "make_report", "report_json", "trident_ledger", "payload_bytes", "default_device",
 ]
 
 I64 = np.int64
@@ -148,6 +148,12 @@ class DeviceCsr:
 
     def check(self) -> None:
         check(_capi.lib().spg_csr_check(self.dev.ctx, self.h))
+
+    def checksum(self):
+        """report.cpp:11-26 result_checksum on the device -> (nnz, hash)."""
+        n, h = C.c_int64(), C.c_uint64()
+        check(_capi.lib().spg_result_checksum(self.dev.ctx, self.h, C.byref(n), C.byref(h)))
+        return n.value, h.value
 
     def free(self) -> None:
         if self.h and self.h.value:
@@ -636,6 +642,7 @@ class DriverResult:
     timeline: np.ndarray
     makespan: float
     rounds: int
+    checksum: tuple | None = None  # (nnz, hash) of C, result_checksum computed on the device
 
 
 def _devices_for(procs: int):
@@ -665,11 +672,13 @@ def _run_driver(fn, a, b, procs, lam, scheme, cmap, rounds, topo) -> DriverResul
     tl = (C.c_double * (procs * rounds * 4))()
     check(fn(ctxs, nctx, ha, hb, procs, lam, topo.index_width, topo.value_width, hc, cells, tl))
     dc = [DeviceCsr(devs[r % nctx], hc[r]) for r in range(procs)]
-    c = devs[0].reassemble(dc, cmap).download()
+    gc = devs[0].reassemble(dc, cmap)
+    cs = gc.checksum()
+    c = gc.download()
     led = np.array([[x.messages, x.nnz, x.bytes] for x in cells], np.uint64).reshape(procs, 2, 2, 3)
     tla = np.ctypeslib.as_array(tl).reshape(procs, rounds, 4).copy()
     makespan = float((tla[:, :, 1:].sum(axis=(1, 2))).max()) * 1e-3
-    return DriverResult(c, led, tla, makespan, rounds)
+    return DriverResult(c, led, tla, makespan, rounds, cs)
 
 
 def trident_spgemm(a, b, grid: TridentGrid, topo: TopologySpec | None = None) -> DriverResult:
@@ -703,6 +712,60 @@ def oned_spgemm(a, b, procs: int, gpus_per_node: int, topo: TopologySpec | None 
     topo = topo or TopologySpec(gpus_per_node)
     cmap = make_tile_map(int(a.nrows), int(b.ncols), "rows1d", procs, 1)
     return _run_driver(_capi.lib().spg_oned_spgemm, a, b, procs, gpus_per_node, "rows1d", cmap, 1, topo)
+
+
+def make_report(dr: DriverResult, algo: str, procs: int, gpus_per_node: int, topo: TopologySpec | None = None,
+                matrix_a: str = "", matrix_b: str = "", square: bool = False, seed: int = 0,
+                tilemap: TileMap | None = None, verified: bool | None = None) -> dict:
+    """RunReport (report.hpp, report.cpp:34-99) of a MEASURED run, same keys as
+    the reference's to_json: config, rounds, makespan_seconds (measured device
+    time, not the alpha-beta model), aggregate and per_process ledger,
+    result {nrows, ncols, nnz, checksum} (result_checksum computed on the
+    device), verified, tilemap. Added: "timeline" — per rank and round the
+    measured [exchange_ms, exposed_wait_ms, multiply_ms, merge_ms], so measured
+    timelines can be diffed against the modeled schedule."""
+    topo = topo or TopologySpec(gpus_per_node)
+    L = np.asarray(dr.ledger, np.uint64)
+    P = L.shape[0]
+    GI, LI = 1, 0
+    rep = {"config": {"algo": algo, "procs": procs, "gpus_per_node": gpus_per_node, "matrix_a": matrix_a,
+                      "matrix_b": matrix_b, "square": square, "seed": seed,
+                      "topology": {"nodes": max(1, procs // max(1, gpus_per_node)), "gpus_per_node": gpus_per_node,
+                                   "alpha_li": None, "alpha_gi": None, "beta_li": None, "beta_gi": None,
+                                   "index_width": topo.index_width, "value_width": topo.value_width}},
+           "rounds": dr.rounds, "makespan_seconds": dr.makespan}
+    rep["aggregate"] = {name: {"messages": int(L[:, 0, c, 0].sum()), "nnz_sent": int(L[:, 0, c, 1].sum()),
+                               "bytes_sent": int(L[:, 0, c, 2].sum())} for name, c in (("gi", GI), ("li", LI))}
+    per = []
+    done = np.asarray(dr.timeline)[:, :, 1:].sum(axis=(1, 2)) * 1e-3
+    for r in range(P):
+        row = {"rank": r, "node": r // max(1, gpus_per_node)}
+        for pfx, c in (("gi_", GI), ("li_", LI)):
+            row[pfx + "messages"] = int(L[r, 0, c, 0])
+            row[pfx + "nnz_sent"] = int(L[r, 0, c, 1])
+            row[pfx + "bytes_sent"] = int(L[r, 0, c, 2])
+            row[pfx + "nnz_recv"] = int(L[r, 1, c, 1])
+            row[pfx + "bytes_recv"] = int(L[r, 1, c, 2])
+        row["completion_time"] = float(done[r])
+        per.append(row)
+    rep["per_process"] = per
+    nnz, h = dr.checksum if dr.checksum is not None else (int(dr.c.nnz), None)
+    rep["result"] = {"nrows": int(dr.c.nrows), "ncols": int(dr.c.ncols), "nnz": int(nnz),
+                     "checksum": None if h is None else f"0x{h:016x}"}
+    rep["verified"] = verified
+    if tilemap is not None:
+        rep["tilemap"] = {"scheme": tilemap.scheme, "procs": tilemap.procs, "gpus_per_node": tilemap.gpus_per_node,
+                          "nrows": tilemap.nrows, "ncols": tilemap.ncols,
+                          "row_bounds": [int(x) for x in tilemap.row_bounds],
+                          "col_bounds": [int(x) for x in tilemap.col_bounds]}
+    rep["timeline"] = [[[float(x) for x in rnd] for rnd in rank] for rank in np.asarray(dr.timeline)]
+    return rep
+
+
+def report_json(rep: dict) -> str:
+    """RunReport::to_json layout (two-space indent, keys in the reference's order)."""
+    import json
+    return json.dumps(rep, indent=2)
 
 
 def run_algo(algo: str, a, b, procs: int, gpus_per_node: int, topo: TopologySpec | None = None) -> DriverResult:

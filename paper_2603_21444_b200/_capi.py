@@ -17,7 +17,7 @@ CXX_LIB_PATH = os.path.join(_HERE, "lib", "libspgsim_b200.so")
 EXPORTS = [
     "spg_last_error", "spg_version", "spg_device_count", "spg_init", "spg_finalize", "spg_ctx_stream", "spg_ctx_synchronize",
     "spg_ctx_device", "spg_timing_enable", "spg_timing_reset", "spg_timing_read", "spg_csr_upload",
-    "spg_csr_zeros", "spg_csr_shape", "spg_csr_upload_into", "spg_csr_download", "spg_csr_check", "spg_csr_free",
+    "spg_csr_zeros", "spg_csr_shape", "spg_csr_upload_into", "spg_csr_download", "spg_csr_check", "spg_csr_free", "spg_result_checksum",
     "spg_csr_device_ptrs", "spg_spgemm", "spg_spgemm_products", "spg_spgeam", "spg_spgeam_inplace",
     "spg_vconcat", "spg_csr_extract", "spg_csr_copy", "spg_tile_rects", "spg_partition", "spg_reassemble", "spg_spgemm_host", "spg_column_normalize", "spg_prune", "spg_elementwise_power", "spg_mcl_poststep",
     "spg_trident_grid", "spg_trident_spgemm", "spg_summa_spgemm", "spg_oned_spgemm",
@@ -76,6 +76,7 @@ def lib() -> C.CDLL:
         "spg_spgeam_inplace": (st, [vp, P(vp), vp]),
         "spg_vconcat": (st, [vp, P(vp), i32, P(vp)]),
         "spg_csr_extract": (st, [vp, vp, i64, i64, i64, i64, P(vp)]),
+        "spg_result_checksum": (st, [vp, vp, P(i64), P(C.c_uint64)]),
         "spg_tile_rects": (st, [i64, i64, i32, i32, i32, P(i64)]),
         "spg_partition": (st, [P(vp), i32, vp, i32, i32, i32, P(vp)]),
         "spg_reassemble": (st, [vp, P(vp), i32, i64, i64, i32, i32, i32, P(vp)]),

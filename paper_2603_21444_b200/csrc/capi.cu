@@ -423,6 +423,17 @@ spg_status spg_csr_copy(spg_ctx* ctx, const spg_csr* m, spg_csr** out) {
     });
 }
 
+spg_status spg_result_checksum(spg_ctx* ctx, const spg_csr* m, int64_t* nnz, uint64_t* hash) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(m, "m");
+        need(hash, "hash");
+        DeviceScope ds(ctx->device);
+        if (nnz) *nnz = m->nnz;
+        *hash = result_checksum(ctx, m);
+    });
+}
+
 spg_status spg_tile_rects(int64_t nrows, int64_t ncols, int scheme, int procs, int gpus_per_node,
                           int64_t* rects_out) {
     return guard([&] {

@@ -351,6 +351,37 @@ __global__ void k_power(double* __restrict__ val, int64_t nnz, double r) {
     GRID_STRIDE(t, nnz) val[t] = mcl_power(val[t], r);
 }
 
+// ---------------------------------------------------------- result checksum
+// report.cpp:11-26: Σ (mod 2^64) over entries of
+// mix64(mix64(mix64(row + K) ^ col) ^ llround(v * 1e9)) — order-independent
+// integer work, so the device sum equals the reference's exactly. 8 lanes per
+// row, per-thread partial sums, one atomic per warp.
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+__global__ void k_checksum(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                           const double* __restrict__ val, int64_t m, unsigned long long* __restrict__ out) {
+    constexpr int G = 8;
+    const int lane = threadIdx.x & (G - 1);
+    const int64_t g0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) / G;
+    const int64_t ng = (int64_t(gridDim.x) * blockDim.x) / G;
+    uint64_t acc = 0;
+    for (int64_t i = g0; i < m; i += ng) {
+        const uint64_t hr = mix64(static_cast<uint64_t>(i) + 0x51ED270B9A3E51EBull);
+        for (int64_t t = rp[i] + lane; t < rp[i + 1]; t += G) {
+            const long long q = llround(__dmul_rn(val[t], 1e9));
+            uint64_t h = mix64(hr ^ static_cast<uint64_t>(static_cast<int64_t>(col[t])));
+            acc += mix64(h ^ static_cast<uint64_t>(q));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, static_cast<unsigned long long>(acc));
+}
+
 // -------------------------------------------------------- canonical check
 // err[0] = first offending row (or INT64_MAX), err[1] = violation code.
 __global__ void k_check(const int64_t* __restrict__ rp, const int32_t* __restrict__ col, int64_t m, int64_t ncols,
@@ -770,6 +801,20 @@ spg_csr* mcl_poststep(spg_ctx* ctx, const spg_csr* c, double th, double r) {
         throw;
     }
     return out;
+}
+
+uint64_t result_checksum(spg_ctx* ctx, const spg_csr* m) {
+    DBuf<unsigned long long> d(ctx, 1);
+    SPG_CUDA(cudaMemsetAsync(d.p, 0, sizeof(unsigned long long), ctx->stream));
+    if (m->nrows && m->nnz) {
+        KTime kt(ctx, "result_checksum");
+        k_checksum<<<grid_for(ctx, m->nrows * 8), 256, 0, ctx->stream>>>(m->rowptr, m->colind, m->values, m->nrows, d);
+        SPG_LAUNCH_CHECK();
+    }
+    unsigned long long h = 0;
+    SPG_CUDA(cudaMemcpyAsync(&h, d.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return h;
 }
 
 void check_canonical(spg_ctx* ctx, const spg_csr* m) {

@@ -203,6 +203,8 @@ void elementwise_power(spg_ctx* ctx, spg_csr* m, double exponent);
 // One MCL iteration's post-step (apps.cpp:79-82): column_normalize(power(prune(column_normalize(c))))
 spg_csr* mcl_poststep(spg_ctx* ctx, const spg_csr* c, double prune_threshold, double inflation);
 void check_canonical(spg_ctx* ctx, const spg_csr* m);
+// report.cpp:11-26 result_checksum hash (order-independent, exact)
+uint64_t result_checksum(spg_ctx* ctx, const spg_csr* m);
 
 // Exclusive scan of n int64 counts into out[0..n] (out[n] = total). In-place allowed.
 void exclusive_scan_i64(spg_ctx* ctx, const int64_t* in, int64_t* out, int64_t n);

@@ -139,3 +139,42 @@ def test_capi_tile_rects_grid_errors():
     with pytest.raises(spg.SpgError) as e:
         spg.tile_rects(4, 4, "bogus", 4, 1)
     assert e.value.kind == "ParameterError"
+
+
+REPORT_KEYS = ["config", "rounds", "makespan_seconds", "aggregate", "per_process", "result", "verified"]
+PER_PROCESS_KEYS = ["rank", "node"] + [p + k for p in ("gi_", "li_") for k in
+                                       ("messages", "nnz_sent", "bytes_sent", "nnz_recv", "bytes_recv")] + \
+    ["completion_time"]
+
+
+def test_make_report_layout_and_ledger_fields():
+    # RunReport::to_json key order (report.cpp:34-83) filled from a measured result
+    import json
+    P, lam = 8, 2
+    a = csr("er300_p3_A")
+    g = spg.TridentGrid.create(P, lam)
+    L = z()[f"trident_P{P}_L{lam}_ledger"]
+    tl = np.arange(P * g.q * 4, dtype=np.float64).reshape(P, g.q, 4)
+    dr = spg.DriverResult(a, L, tl, 1.25, g.q, (int(a.nnz), 0xDEADBEEF))
+    tm = spg.make_tile_map(300, 300, "trident", P, lam)
+    rep = spg.make_report(dr, "trident", P, lam, tilemap=tm, verified=True)
+    assert list(rep)[:len(REPORT_KEYS)] == REPORT_KEYS and "tilemap" in rep and "timeline" in rep
+    assert [list(r) for r in rep["per_process"]] == [PER_PROCESS_KEYS] * P
+    for r, row in enumerate(rep["per_process"]):
+        assert row["gi_bytes_recv"] == int(L[r, 1, 1, 2]) and row["li_nnz_sent"] == int(L[r, 0, 0, 1])
+        assert row["completion_time"] == pytest.approx(tl[r, :, 1:].sum() * 1e-3)
+    assert rep["aggregate"]["gi"]["bytes_sent"] == int(L[:, 0, 1, 2].sum())
+    assert rep["result"] == {"nrows": 300, "ncols": 300, "nnz": int(a.nnz), "checksum": "0x00000000deadbeef"}
+    assert json.loads(spg.report_json(rep)) == rep
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_port_result_checksum_vs_reference():
+    # report.cpp:11-26, incl. negative values, halves and an empty matrix
+    for s in (1, 2):
+        a = O.port_gen_erdos_renyi(500, 0.02, s)
+        assert O.port_result_checksum(a) == O.ref_result_checksum(a)
+    m = O.Csr(3, 4, np.array([0, 2, 2, 5], np.int64), np.array([0, 3, 1, 2, 3], np.int64),
+              np.array([-1.5e-9, 2.5e-9, -0.25, 7.0, 0.0]))
+    assert O.port_result_checksum(m) == O.ref_result_checksum(m)
+    assert O.port_result_checksum(spg.CsrMatrix.zeros(5, 5)) == O.ref_result_checksum(spg.CsrMatrix.zeros(5, 5))
