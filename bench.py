@@ -285,21 +285,41 @@ def ours_single(args):
     for arr in (c_rp, c_ci, c_va):
         _capi.check(L.spg_host_register(arr.ctypes.data, arr.nbytes))
 
-    def e2e_step():
+    def e2e_two_calls():
         h = C.c_void_p()
         _capi.check(L.spg_spgemm_host(dev.ctx, m, a.ncols, rp.ctypes.data, ci.ctypes.data, va.ctypes.data, m,
                                       a.ncols, rp.ctypes.data, ci.ctypes.data, va.ctypes.data, 4, C.byref(h)))
         _capi.check(L.spg_csr_download(dev.ctx, h, c_rp.ctypes.data, c_ci.ctypes.data, 4, c_va.ctypes.data))
         _capi.check(L.spg_csr_free(h))
 
+    h2h_batches = int(os.environ.get("SPG_H2H_BATCHES", 1))
+
+    def e2e_host_to_host():
+        got = C.c_int64()
+        _capi.check(L.spg_spgemm_host_to_host(dev.ctx, m, a.ncols, rp.ctypes.data, ci.ctypes.data, va.ctypes.data,
+                                              m, a.ncols, rp.ctypes.data, ci.ctypes.data, va.ctypes.data, 4,
+                                              h2h_batches, nnz_c, c_rp.ctypes.data, c_ci.ctypes.data,
+                                              c_va.ctypes.data, C.byref(got)))
+        assert got.value == nnz_c
+
+    def e2e_time(fn):
+        fn()
+        dev.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            fn()
+        dev.synchronize()
+        return (time.perf_counter() - t0) / e2e_steps * 1e3
+
     e2e_steps = max(1, min(args.steps, int(os.environ.get("SPG_E2E_STEPS", 3))))
-    e2e_step()
-    dev.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        e2e_step()
-    dev.synchronize()
-    e2e_ms = (time.perf_counter() - t0) / e2e_steps * 1e3
+    e2e_ms_two = e2e_time(e2e_two_calls)
+    ref_rp, ref_ci, ref_va = c_rp.copy(), c_ci[::1009].copy(), c_va[::1009].copy()
+    c_rp[:] = -1
+    e2e_ms = e2e_time(e2e_host_to_host)
+    # the host-to-host C must equal the two-call C (row pointers exact, every 1009th entry)
+    if not (np.array_equal(c_rp, ref_rp) and np.array_equal(c_ci[::1009], ref_ci)
+            and np.array_equal(c_va[::1009], ref_va)):
+        raise RuntimeError("spg_spgemm_host_to_host result differs from spg_spgemm_host + spg_csr_download")
     for arr in (rp, ci, va, c_rp, c_ci, c_va):
         L.spg_host_unregister(arr.ctypes.data)
     h2d = rp.nbytes + ci.nbytes + va.nbytes  # C = A*A: the C ABI uploads the shared host matrix once
@@ -326,7 +346,10 @@ def ours_single(args):
         "kernel_ms": {k: round(v[1] / max(1, v[0]), 4) for k, v in own.items()},
         "e2e": {"value": round(2.0 * products / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
                 "ms_per_step": round(e2e_ms, 2), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "spg_spgemm_host + spg_csr_download (C ABI, pinned host buffers)"},
+                "path": f"spg_spgemm_host_to_host (one C ABI call, host CSR in and out, pinned host buffers, "
+                        f"{h2h_batches} row batch(es))",
+                "two_calls_ms_per_step": round(e2e_ms_two, 2),
+                "two_calls_value": round(2.0 * products / (e2e_ms_two * 1e-3) / 1e9, 3)},
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": int(launches),

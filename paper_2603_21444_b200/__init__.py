@@ -212,6 +212,38 @@ class Device:
     def spgemm(self, a: DeviceCsr, b: DeviceCsr) -> DeviceCsr:
         return self._out(_capi.lib().spg_spgemm, a.h, b.h)
 
+    def spgemm_host_to_host(self, a, b, batches: int = 0, cap: int | None = None) -> CsrMatrix:
+        """spgemm_local (csr.cpp:132-165) host to host through spg_spgemm_host_to_host:
+        A in row batches, each batch's download overlapping the next batch's
+        multiply. cap = room for C's entries (default: the product count, an
+        upper bound); retried once with the exact nnz if it was too small."""
+        a, b = CsrMatrix.of(a), CsrMatrix.of(b)
+        same = a is b
+        ar, ac, av = (np.ascontiguousarray(a.rowptr, I64), np.ascontiguousarray(a.colind, I64),
+                      np.ascontiguousarray(a.values, np.float64))
+        br, bc, bv = (ar, ac, av) if same else (np.ascontiguousarray(b.rowptr, I64),
+                                                np.ascontiguousarray(b.colind, I64),
+                                                np.ascontiguousarray(b.values, np.float64))
+        if cap is None:
+            blen = np.diff(br)
+            cap = int(blen[ac].sum()) if len(ac) else 0
+        lib = _capi.lib()
+        for _ in range(2):
+            rp = np.empty(int(a.nrows) + 1, I64)
+            ci = np.empty(max(1, cap), I64)
+            va = np.empty(max(1, cap), np.float64)
+            nnz = C.c_int64()
+            st = lib.spg_spgemm_host_to_host(self.ctx, int(a.nrows), int(a.ncols), _ptr(ar), _ptr(ac) or None,
+                                             _ptr(av) or None, int(b.nrows), int(b.ncols), _ptr(br),
+                                             _ptr(bc) or None, _ptr(bv) or None, 8, int(batches), int(cap),
+                                             _ptr(rp), _ptr(ci), _ptr(va), C.byref(nnz))
+            if st == 0:
+                return CsrMatrix(int(a.nrows), int(b.ncols), rp, ci[:nnz.value].copy(), va[:nnz.value].copy())
+            if nnz.value <= cap:
+                check(st)
+            cap = nnz.value
+        check(st)
+
     def products(self, a: DeviceCsr, b: DeviceCsr) -> int:
         p = C.c_int64()
         check(_capi.lib().spg_spgemm_products(self.ctx, a.h, b.h, C.byref(p)))

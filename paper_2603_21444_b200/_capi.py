@@ -19,7 +19,7 @@ EXPORTS = [
     "spg_ctx_device", "spg_timing_enable", "spg_timing_reset", "spg_timing_read", "spg_csr_upload",
     "spg_csr_zeros", "spg_csr_shape", "spg_csr_upload_into", "spg_csr_download", "spg_csr_check", "spg_csr_free", "spg_result_checksum",
     "spg_csr_device_ptrs", "spg_spgemm", "spg_spgemm_products", "spg_spgeam", "spg_spgeam_inplace",
-    "spg_vconcat", "spg_csr_extract", "spg_csr_copy", "spg_tile_rects", "spg_partition", "spg_reassemble", "spg_spgemm_host", "spg_column_normalize", "spg_prune", "spg_elementwise_power", "spg_mcl_poststep",
+    "spg_vconcat", "spg_csr_extract", "spg_csr_copy", "spg_tile_rects", "spg_partition", "spg_reassemble", "spg_spgemm_host", "spg_spgemm_host_to_host", "spg_column_normalize", "spg_prune", "spg_elementwise_power", "spg_mcl_poststep",
     "spg_trident_grid", "spg_trident_spgemm", "spg_summa_spgemm", "spg_oned_spgemm",
     "spg_host_register", "spg_host_unregister",
     "spg_csr_ipc_export", "spg_csr_ipc_open", "spg_csr_make_shareable", "spg_trident_rank",
@@ -82,6 +82,8 @@ def lib() -> C.CDLL:
         "spg_reassemble": (st, [vp, P(vp), i32, i64, i64, i32, i32, i32, P(vp)]),
         "spg_csr_copy": (st, [vp, vp, P(vp)]),
         "spg_spgemm_host": (st, [vp, i64, i64, vp, vp, vp, i64, i64, vp, vp, vp, i32, P(vp)]),
+        "spg_spgemm_host_to_host": (st, [vp, i64, i64, vp, vp, vp, i64, i64, vp, vp, vp, i32, i32, i64, vp, vp, vp,
+                                         P(i64)]),
         "spg_column_normalize": (st, [vp, vp]),
         "spg_prune": (st, [vp, vp, f64, P(vp)]),
         "spg_elementwise_power": (st, [vp, vp, f64]),

@@ -126,7 +126,7 @@ spg_status spg_init(int device, spg_ctx** out) {
         SPG_CUDA(cudaDeviceGetDefaultMemPool(&ctx->pool, device));
         uint64_t keep = UINT64_MAX;  // keep freed blocks cached in the pool
         SPG_CUDA(cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &keep));
-        SPG_CUDA(cudaMallocHost(&ctx->host_scalars, 64));
+        SPG_CUDA(cudaMallocHost(&ctx->host_scalars, spg_ctx::HOST_SCALAR_BYTES));
         // Peer access to every other device (NVLink P2P for the exchange).
         for (int d = 0; d < n; ++d) {
             if (d == device) continue;
@@ -482,6 +482,54 @@ spg_status spg_spgemm_host(spg_ctx* ctx, int64_t a_nrows, int64_t a_ncols, const
     if (st == SPG_OK && !same)
         st = spg_csr_upload(ctx, b_nrows, b_ncols, b_rowptr, b_colind, colind_width, b_values, &b);
     if (st == SPG_OK) st = spg_spgemm(ctx, a, same ? a : b, c);
+    if (a) spg_csr_free(a);
+    if (b) spg_csr_free(b);
+    return st;
+}
+
+spg_status spg_spgemm_host_to_host(spg_ctx* ctx, int64_t a_nrows, int64_t a_ncols, const int64_t* a_rowptr,
+                                   const void* a_colind, const double* a_values, int64_t b_nrows, int64_t b_ncols,
+                                   const int64_t* b_rowptr, const void* b_colind, const double* b_values,
+                                   int colind_width, int batches, int64_t c_cap, int64_t* c_rowptr,
+                                   void* c_colind, double* c_values, int64_t* c_nnz) {
+    spg_csr *a = nullptr, *b = nullptr;
+    const bool same = a_nrows == b_nrows && a_ncols == b_ncols && a_rowptr == b_rowptr && a_colind == b_colind &&
+                      a_values == b_values;
+    spg_status st = guard([&] {
+        need(ctx, "ctx");
+        need(c_rowptr, "c_rowptr");
+        need(c_nnz, "c_nnz");
+        need(a_rowptr, "a_rowptr");
+        if (c_cap > 0) {
+            need(c_colind, "c_colind");
+            need(c_values, "c_values");
+        }
+        if (colind_width != 4 && colind_width != 8) fail(SPG_PARAMETER_ERROR, "colind_width must be 4 or 8");
+        if (a_ncols != b_nrows) fail(SPG_DIMENSION_ERROR, "spgemm_local: inner dimensions differ");
+    });
+    if (st == SPG_OK) st = spg_csr_upload(ctx, a_nrows, a_ncols, a_rowptr, a_colind, colind_width, a_values, &a);
+    if (st == SPG_OK && !same)
+        st = spg_csr_upload(ctx, b_nrows, b_ncols, b_rowptr, b_colind, colind_width, b_values, &b);
+    if (st == SPG_OK)
+        st = guard([&] {
+            DeviceScope ds(ctx->device);
+            // batch cuts at equal shares of A's entries (host row pointers)
+            const int nb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(batches > 0 ? batches : 1,
+                                                                                   std::max<int64_t>(1, a_nrows))));
+            std::vector<int64_t> cuts(nb + 1, 0);
+            const int64_t nnz = a_rowptr[a_nrows];
+            for (int i = 1; i < nb; ++i) {
+                const int64_t target = nnz / nb * i + (nnz % nb) * i / nb;
+                const int64_t r = std::lower_bound(a_rowptr, a_rowptr + a_nrows + 1, target) - a_rowptr;
+                cuts[i] = std::max(cuts[i - 1], std::min<int64_t>(r, a_nrows));
+            }
+            cuts[nb] = a_nrows;
+            *c_nnz = spgemm_to_host(ctx, a, same ? a : b, cuts.data(), nb, c_rowptr, c_colind, colind_width,
+                                    c_values, c_cap);
+            if (*c_nnz > c_cap)
+                fail(SPG_PARAMETER_ERROR, "spgemm_host_to_host: nnz(C)=" + std::to_string(*c_nnz) +
+                                              " exceeds c_cap=" + std::to_string(c_cap));
+        });
     if (a) spg_csr_free(a);
     if (b) spg_csr_free(b);
     return st;

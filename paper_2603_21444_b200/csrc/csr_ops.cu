@@ -549,10 +549,26 @@ void free_csr(spg_csr* m) {
     delete m;
 }
 
+// Small read-backs are written by a kernel straight into the context's
+// mapped pinned scalars instead of a cudaMemcpy: a D2H copy would queue on the
+// copy engine behind bulk downloads running on other streams (the
+// host-to-host multiply downloads batch i while batch i+1 is multiplied).
+__global__ void k_peek(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+void* peek_async(spg_ctx* ctx, int off, const void* dsrc, int bytes) {
+    if (off < 0 || off + bytes > spg_ctx::HOST_SCALAR_BYTES) fail(SPG_ERROR, "peek_async: slot out of range");
+    unsigned char* dst = reinterpret_cast<unsigned char*>(ctx->host_scalars) + off;
+    k_peek<<<1, 32, 0, ctx->stream>>>(static_cast<const unsigned char*>(dsrc), dst, bytes);
+    SPG_LAUNCH_CHECK();
+    return dst;
+}
+
 int64_t read_scalar(spg_ctx* ctx, const int64_t* dptr) {
-    SPG_CUDA(cudaMemcpyAsync(ctx->host_scalars, dptr, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    peek_async(ctx, 0, dptr, sizeof(int64_t));
     SPG_CUDA(cudaStreamSynchronize(ctx->stream));
-    return ctx->host_scalars[0];
+    return *reinterpret_cast<volatile int64_t*>(ctx->host_scalars);
 }
 
 spg_csr* spgeam(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
@@ -862,6 +878,89 @@ void widen_index(spg_ctx* ctx, const int32_t* d_in, int64_t* d_out, int64_t n) {
     if (n == 0) return;
     k_widen<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(d_in, d_out, n);
     SPG_LAUNCH_CHECK();
+}
+
+// C = A*B straight into host arrays (the reference's spgemm_local returns C
+// by value, csr.cpp:132-165). A is multiplied in row batches (cuts[0..nb]);
+// batch i's columns/values go down the host link on the aux streams while
+// batch i+1 is multiplied on the context stream, so only the last batch's
+// download is exposed. Row pointers are rebased into one device array and
+// fetched at the end. Batch products stay alive until every copy is done.
+int64_t spgemm_to_host(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const int64_t* cuts, int nb,
+                       int64_t* h_rowptr, void* h_colind, int colind_width, double* h_values, int64_t cap) {
+    if (a->ncols != b->nrows) fail(SPG_DIMENSION_ERROR, "spgemm: inner dimensions differ");
+    constexpr size_t CH = size_t(64) << 20;
+    const int64_t m = a->nrows;
+    DBuf<int64_t> rp(ctx, m + 1);
+    SPG_CUDA(cudaMemsetAsync(rp.get(), 0, sizeof(int64_t), ctx->stream));
+    std::vector<spg_csr*> parts;
+    std::vector<int64_t*> wide;
+    std::vector<cudaEvent_t> evs;
+    int64_t off = 0;
+    int chunk = 0;
+    auto cleanup = [&] {
+        for (int i = 0; i < spg_ctx::NAUX; ++i) cudaStreamSynchronize(ctx->aux[i]);
+        cudaStreamSynchronize(ctx->stream);
+        for (auto* p : wide) dfree(ctx, p);
+        for (auto* p : parts) free_csr(p);
+        for (auto e : evs) cudaEventDestroy(e);
+    };
+    try {
+        for (int i = 0; i < nb; ++i) {
+            const int64_t r0 = cuts[i], r1 = cuts[i + 1];
+            if (r1 <= r0) continue;
+            spg_csr* sub = extract(ctx, a, r0, r1, 0, a->ncols);
+            spg_csr* c = nullptr;
+            try {
+                c = spgemm(ctx, sub, b);
+            } catch (...) {
+                free_csr(sub);
+                throw;
+            }
+            free_csr(sub);
+            parts.push_back(c);
+            {
+                KTime kt(ctx, "rebase_rowptr");
+                k_rebase_rowptr<<<grid_for(ctx, r1 - r0), 256, 0, ctx->stream>>>(c->rowptr, r1 - r0, off,
+                                                                                rp.get() + r0 + 1);
+                SPG_LAUNCH_CHECK();
+            }
+            const int64_t n = c->nnz;
+            if (off + n <= cap && n > 0) {
+                const void* csrc = c->colind;
+                size_t cw = sizeof(int32_t);
+                if (colind_width == 8) {
+                    int64_t* w = dalloc<int64_t>(ctx, n);
+                    wide.push_back(w);
+                    widen_index(ctx, c->colind, w, n);
+                    csrc = w;
+                    cw = sizeof(int64_t);
+                }
+                cudaEvent_t ev;
+                SPG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                evs.push_back(ev);
+                SPG_CUDA(cudaEventRecord(ev, ctx->stream));
+                for (int s = 0; s < spg_ctx::NAUX; ++s) SPG_CUDA(cudaStreamWaitEvent(ctx->aux[s], ev, 0));
+                auto down = [&](void* dst, const void* src, size_t bytes) {
+                    for (size_t o = 0; o < bytes; o += CH, ++chunk)
+                        SPG_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                                                 std::min(CH, bytes - o), cudaMemcpyDeviceToHost,
+                                                 ctx->aux[chunk % spg_ctx::NAUX]));
+                };
+                down(static_cast<char*>(h_colind) + off * cw, csrc, n * cw);
+                down(h_values + off, c->values, n * sizeof(double));
+            }
+            off += n;
+        }
+        if (off <= cap) SPG_CUDA(cudaMemcpyAsync(h_rowptr, rp.get(), (m + 1) * sizeof(int64_t),
+                                                 cudaMemcpyDeviceToHost, ctx->stream));
+    } catch (...) {
+        cleanup();
+        throw;
+    }
+    cleanup();
+    SPG_CUDA(cudaGetLastError());
+    return off;
 }
 
 }  // namespace spgb

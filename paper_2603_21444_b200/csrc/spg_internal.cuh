@@ -64,6 +64,7 @@ struct spg_ctx {
     size_t l2_bytes = 0;
     spgb::Timer timer;
     // Pinned host staging for small scalar read-backs.
+    static constexpr int HOST_SCALAR_BYTES = 256;
     int64_t* host_scalars = nullptr;
     bool tile_attr_set = false;
     // fork/join streams for concurrent slice copies (vconcat pulls from several peers at once)
@@ -171,6 +172,10 @@ void big_cache_release(spg_ctx* ctx);
 // live contexts per device (the block cache's byte budget is shared among them)
 void ctx_live(int device, int delta);
 int64_t read_scalar(spg_ctx* ctx, const int64_t* dptr);
+// Enqueue a kernel copy of `bytes` device bytes into the context's pinned
+// scalars at byte offset `off` (slot 0-7 belongs to read_scalar); returns the
+// host address, valid after the next synchronisation of ctx->stream.
+void* peek_async(spg_ctx* ctx, int off, const void* dsrc, int bytes);
 
 // Kernels (spgemm.cu / spgeam.cu / misc.cu)
 // b_data: when set, B's column/value arrays are complete only at this event
@@ -185,6 +190,11 @@ spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n, cudaEvent_t 
 spg_csr* hconcat(spg_ctx* ctx, const spg_csr* const* parts, int n);
 spg_csr* extract(spg_ctx* ctx, const spg_csr* m, int64_t r0, int64_t r1, int64_t c0, int64_t c1);
 spg_csr* copy_csr(spg_ctx* ctx, const spg_csr* m);
+// C = A*B into host arrays, A in row batches cuts[0..nb] with each batch's
+// download overlapping the next batch's multiply. Returns nnz(C); nothing but
+// the count is written when it exceeds cap.
+int64_t spgemm_to_host(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const int64_t* cuts, int nb,
+                       int64_t* h_rowptr, void* h_colind, int colind_width, double* h_values, int64_t cap);
 
 // Device tile store (tiles.cu): make_tile_map rectangles (partition.cpp:95-159),
 // partition (:161-222) onto the tiles' devices, reassemble (:224-261).

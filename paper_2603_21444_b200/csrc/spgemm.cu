@@ -2001,10 +2001,8 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEven
     // 2: tile starts (weight windows; BIG rows alone)
     DBuf<int64_t> wpre(ctx, m + 1), flag(ctx, m), fpos(ctx, m + 1);
     exclusive_scan_i64(ctx, wt, wpre, m);
-    int32_t hc[2];
-    int64_t products = 0;
-    SPG_CUDA(cudaMemcpyAsync(hc, counts.get(), sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
-    SPG_CUDA(cudaMemcpyAsync(&products, total.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    const volatile int32_t* hc = static_cast<int32_t*>(peek_async(ctx, 64, counts.get(), 2 * sizeof(int32_t)));
+    const volatile int64_t* hprod = static_cast<int64_t*>(peek_async(ctx, 72, total.get(), sizeof(int64_t)));
     {
         KTime kt(ctx, "tile_setup");
         k_tile_flags<<<grid_for(ctx, m), 256, 0, ctx->stream>>>(wpre, kind, m, flag);
@@ -2014,6 +2012,7 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEven
     SPG_CUDA(cudaStreamSynchronize(ctx->stream));
     hprof.mark("sync1");
     const int ncta = hc[0], nheavy = hc[1];
+    const int64_t products = *hprod;
     // B's columns and values may still be arriving (trident pulls): everything
     // above read only B's row pointers
     if (b_data) SPG_CUDA(cudaStreamWaitEvent(ctx->stream, b_data, 0));
