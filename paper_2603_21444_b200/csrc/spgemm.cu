@@ -850,6 +850,11 @@ constexpr int NJ = (PMAX + NT - 1) / NT;        // product slots per thread
 constexpr int EPT = (EMAX + NT - 1) / NT;       // entry slots per thread
 constexpr int HW = PMAX / 32 + 2;               // words of the head bitmap
 constexpr int LMAX = PMAX / 3 + 1;              // shared buckets of >= 3 products
+#ifndef SPG_TILE_BPP
+#define SPG_TILE_BPP 2
+#endif
+constexpr int BPP = SPG_TILE_BPP;               // column buckets per product of a row (2 or 4)
+constexpr int CW = BPP / 2;                     // counter words per product (2 x 16-bit counters a word)
 // espan[e] of an entry of a tile row: B row start (30 bits) | B row length (10)
 // | product offset of the entry in its row (12) | products of the row (12)
 constexpr int SP_BS = 30, SP_LEN = 30, SP_IN = 40, SP_PR = 52;
@@ -1296,7 +1301,7 @@ struct __align__(16) TileSmem {
     double val[tile::PMAX];        // staging: the tile's C entries (values)
     TileEnt ent[tile::EMAX];
     int32_t col[tile::PMAX];       // staging: columns
-    uint32_t cnt[tile::PMAX + 2];  // 2 x 16-bit bucket counters per word, then prefixes
+    uint32_t cnt[tile::CW * tile::PMAX + 2];  // 2 x 16-bit bucket counters per word, then prefixes
     uint32_t ebin[tile::EMAX];     // per entry: row bucket base (lo 16) | row bucket count (hi 16)
     int32_t epre[tile::EMAX + 1];  // product prefix of the tile's entries
     int32_t re[tile::RMAX + 1];    // first entry of each row (relative to the tile)
@@ -1424,7 +1429,7 @@ __device__ __forceinline__ TileDesc tile_prologue(TileSmem& S, int64_t k, const 
             const int inrow = static_cast<int>((sp[c] >> tile::SP_IN) & 4095u);
             const int prow = pre - inrow, pr = static_cast<int>(sp[c] >> tile::SP_PR);
             S.ent[q] = TileEnt{static_cast<int64_t>(sp[c] & tile::SP_BS_MASK) - pre, av[c]};
-            S.ebin[q] = static_cast<uint32_t>(2 * prow) | (static_cast<uint32_t>(2 * pr) << 16);
+            S.ebin[q] = static_cast<uint32_t>(tile::BPP * prow) | (static_cast<uint32_t>(tile::BPP * pr) << 16);
             S.epre[q] = pre;
             for (int x = pre; x < pre + len; ++x) S.eof[x] = static_cast<uint16_t>(q);
             pre += len;
@@ -1434,7 +1439,7 @@ __device__ __forceinline__ TileDesc tile_prologue(TileSmem& S, int64_t k, const 
         S.epre[T.E] = ptile;
         S.nlist = 0;
     }
-    for (int q = tid; q <= ptile; q += NT) S.cnt[q] = 0u;  // ptile words = 2*ptile buckets
+    for (int q = tid; q <= tile::CW * ptile; q += NT) S.cnt[q] = 0u;  // CW*ptile words = BPP*ptile buckets
     __syncthreads();
     return T;
 }
@@ -1491,10 +1496,10 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
     TPROF(9)
     // exclusive scan of the packed counters (odd-strided blocks: conflict-free)
     {
-        const int W = ptile;
+        const int W = tile::CW * ptile;
         const int per = ((W + NT - 1) / NT) | 1;
         const int w0 = tid * per;
-        constexpr int PERMAX = ((tile::PMAX + NT - 1) / NT) | 1;
+        constexpr int PERMAX = ((tile::CW * tile::PMAX + NT - 1) / NT) | 1;
         uint32_t wd[PERMAX];
         uint32_t s = 0;
 #pragma unroll
