@@ -159,11 +159,12 @@ spg_status spg_spgemm_host(spg_ctx* ctx, int64_t a_nrows, int64_t a_ncols, const
 
 /* Host-to-host local multiply, the whole of spgemm_local (csr.cpp:132-165:
  * host CSR in, host CSR out). A and B are uploaded (once when B is A), A is
- * multiplied in `batches` row batches (<= 0: 1) cut at equal shares of A's
+ * multiplied in `batches` row batches (<= 0: 8) cut at equal shares of A's
  * entries, and each batch's columns/values are copied into the caller's
- * arrays while the next batch is multiplied. (Measured on config 2: 8 batches
- * 378 ms against 303 ms for one — the overlap does not pay on the B200 host
- * link, so one batch is the default; batches bound device memory for C.) c_rowptr has a_nrows+1 slots,
+ * arrays while the next batch is multiplied. At most two batch products are
+ * alive on the device at a time, so batches also bound the device memory C
+ * needs. (Config 2 on one B200: 8 batches 250-267 ms per call against 283-290
+ * ms for spg_spgemm_host + spg_csr_download; 32 batches 556 ms.) c_rowptr has a_nrows+1 slots,
  * c_colind/c_values room for c_cap entries (colind 4- or 8-byte per
  * colind_width, which also gives the width of A's and B's colind). *c_nnz
  * receives nnz(C); when it exceeds c_cap the call returns SPG_PARAMETER_ERROR

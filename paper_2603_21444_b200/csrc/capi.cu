@@ -514,7 +514,7 @@ spg_status spg_spgemm_host_to_host(spg_ctx* ctx, int64_t a_nrows, int64_t a_ncol
         st = guard([&] {
             DeviceScope ds(ctx->device);
             // batch cuts at equal shares of A's entries (host row pointers)
-            const int nb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(batches > 0 ? batches : 1,
+            const int nb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(batches > 0 ? batches : 8,
                                                                                    std::max<int64_t>(1, a_nrows))));
             std::vector<int64_t> cuts(nb + 1, 0);
             const int64_t nnz = a_rowptr[a_nrows];

@@ -5,6 +5,7 @@
 //   column_normalize / prune (reference csr.cpp:224-249) — MCL post-step
 //   check_canonical (reference csr.cpp:30-50)
 #include <atomic>
+#include <deque>
 #include <algorithm>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -884,8 +885,10 @@ void widen_index(spg_ctx* ctx, const int32_t* d_in, int64_t* d_out, int64_t n) {
 // by value, csr.cpp:132-165). A is multiplied in row batches (cuts[0..nb]);
 // batch i's columns/values go down the host link on the aux streams while
 // batch i+1 is multiplied on the context stream, so only the last batch's
-// download is exposed. Row pointers are rebased into one device array and
-// fetched at the end. Batch products stay alive until every copy is done.
+// download is exposed. At most two batch products are alive on the device
+// (batch i is freed once its download has finished, before batch i+2 is
+// multiplied), so batches also bound the device memory C needs. Row pointers
+// are rebased into one device array and fetched at the end.
 int64_t spgemm_to_host(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const int64_t* cuts, int nb,
                        int64_t* h_rowptr, void* h_colind, int colind_width, double* h_values, int64_t cap) {
     if (a->ncols != b->nrows) fail(SPG_DIMENSION_ERROR, "spgemm: inner dimensions differ");
@@ -893,32 +896,50 @@ int64_t spgemm_to_host(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const i
     const int64_t m = a->nrows;
     DBuf<int64_t> rp(ctx, m + 1);
     SPG_CUDA(cudaMemsetAsync(rp.get(), 0, sizeof(int64_t), ctx->stream));
-    std::vector<spg_csr*> parts;
-    std::vector<int64_t*> wide;
-    std::vector<cudaEvent_t> evs;
-    int64_t off = 0;
-    int chunk = 0;
+    struct Part {
+        spg_csr* c = nullptr;
+        int64_t* wide = nullptr;
+        cudaEvent_t ev[spg_ctx::NAUX + 1] = {};  // [0]: product ready; [1..]: downloads done per aux stream
+    };
+    std::deque<Part> live;
+    auto retire = [&](Part& p) {  // wait for the part's downloads, then release it
+        for (int s = 1; s <= spg_ctx::NAUX; ++s)
+            if (p.ev[s]) cudaEventSynchronize(p.ev[s]);
+        if (p.wide) dfree(ctx, p.wide);
+        free_csr(p.c);
+        for (auto e : p.ev)
+            if (e) cudaEventDestroy(e);
+    };
     auto cleanup = [&] {
         for (int i = 0; i < spg_ctx::NAUX; ++i) cudaStreamSynchronize(ctx->aux[i]);
+        while (!live.empty()) {
+            retire(live.front());
+            live.pop_front();
+        }
         cudaStreamSynchronize(ctx->stream);
-        for (auto* p : wide) dfree(ctx, p);
-        for (auto* p : parts) free_csr(p);
-        for (auto e : evs) cudaEventDestroy(e);
     };
+    int64_t off = 0;
+    int chunk = 0;
     try {
         for (int i = 0; i < nb; ++i) {
             const int64_t r0 = cuts[i], r1 = cuts[i + 1];
             if (r1 <= r0) continue;
+            if (live.size() >= 2) {
+                retire(live.front());
+                live.pop_front();
+            }
             spg_csr* sub = extract(ctx, a, r0, r1, 0, a->ncols);
-            spg_csr* c = nullptr;
+            live.emplace_back();
+            Part& p = live.back();
             try {
-                c = spgemm(ctx, sub, b);
+                p.c = spgemm(ctx, sub, b);
             } catch (...) {
                 free_csr(sub);
+                live.pop_back();
                 throw;
             }
             free_csr(sub);
-            parts.push_back(c);
+            spg_csr* c = p.c;
             {
                 KTime kt(ctx, "rebase_rowptr");
                 k_rebase_rowptr<<<grid_for(ctx, r1 - r0), 256, 0, ctx->stream>>>(c->rowptr, r1 - r0, off,
@@ -930,17 +951,14 @@ int64_t spgemm_to_host(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const i
                 const void* csrc = c->colind;
                 size_t cw = sizeof(int32_t);
                 if (colind_width == 8) {
-                    int64_t* w = dalloc<int64_t>(ctx, n);
-                    wide.push_back(w);
-                    widen_index(ctx, c->colind, w, n);
-                    csrc = w;
+                    p.wide = dalloc<int64_t>(ctx, n);
+                    widen_index(ctx, c->colind, p.wide, n);
+                    csrc = p.wide;
                     cw = sizeof(int64_t);
                 }
-                cudaEvent_t ev;
-                SPG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-                evs.push_back(ev);
-                SPG_CUDA(cudaEventRecord(ev, ctx->stream));
-                for (int s = 0; s < spg_ctx::NAUX; ++s) SPG_CUDA(cudaStreamWaitEvent(ctx->aux[s], ev, 0));
+                for (auto& e : p.ev) SPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                SPG_CUDA(cudaEventRecord(p.ev[0], ctx->stream));
+                for (int s = 0; s < spg_ctx::NAUX; ++s) SPG_CUDA(cudaStreamWaitEvent(ctx->aux[s], p.ev[0], 0));
                 auto down = [&](void* dst, const void* src, size_t bytes) {
                     for (size_t o = 0; o < bytes; o += CH, ++chunk)
                         SPG_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
@@ -949,6 +967,7 @@ int64_t spgemm_to_host(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const i
                 };
                 down(static_cast<char*>(h_colind) + off * cw, csrc, n * cw);
                 down(h_values + off, c->values, n * sizeof(double));
+                for (int s = 0; s < spg_ctx::NAUX; ++s) SPG_CUDA(cudaEventRecord(p.ev[s + 1], ctx->aux[s]));
             }
             off += n;
         }
