@@ -1730,12 +1730,22 @@ __global__ void __launch_bounds__(tile::NT, SPG_TILE_MINB) k_tile(
     TileDesc T = tile_prologue(S, k0, arp, aval, espan, tr, te);
     if (!T.big) tile_gather<NJ>(S, T.ptile, bcol, bval, col, val, aux);
     while (true) {
+#ifdef SPG_TICKET_SMEM
         if (tid == 0) S.ticket = static_cast<int64_t>(atomicAdd(ticket, 1ull));
+#else
+        // the next ticket stays in thread 0's register while the tile is
+        // processed: its round trip is only waited for at the publish barrier
+        unsigned long long tk = 0;
+        if (tid == 0) tk = atomicAdd(ticket, 1ull);
+#endif
         TPROF(0)
         const int nnz = T.big ? 0 : tile_process<NJ>(S, T, cshift, col, val, aux);
         TPROF(1)
         const int64_t agg = T.big ? side_nnz[T.r0] : static_cast<int64_t>(nnz);
         if (tid == 0) st_status(status + T.k, (T.k == 0 ? ST_INC : ST_AGG) | static_cast<uint64_t>(agg));
+#ifndef SPG_TICKET_SMEM
+        if (tid == 0) S.ticket = static_cast<int64_t>(tk);
+#endif
         __syncthreads();  // staging + rend complete, ticket visible
         TPROF(2)
         const TileDesc F = T;  // tile to finish
