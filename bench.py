@@ -271,7 +271,7 @@ def ours_single(args):
     kt = dev.timing_read()
     own = {k: v for k, v in kt.items()}
     launches = sum(v[0] for v in own.values())
-    kname = "spgemm_tile" if "spgemm_tile" in own else "spgemm_numeric"
+    kname = "spgemm_merge"
     num_ms = own.get(kname, (1, 0.0))[1] / max(1, own.get(kname, (1, 0))[0])
     dev.timing(False)
 
@@ -341,8 +341,8 @@ def ours_single(args):
         "config": {"workload": CONFIGS[args.config]["desc"], "config_id": args.config, "grid": "P=1 lambda=1 q=1",
                    "products": products, "nnz_A": nnz_a, "nnz_C": nnz_c,
                    "l2": "inputs (1.6 GB) and C (12.9 GB) larger than the 126 MB L2; no flush"},
-        "roofline": {"bound": "hbm", "kernel": "k_tile (single-pass tile multiply: gather, sort, look-back, write C)"
-                     if kname == "spgemm_tile" else "spgemm_numeric (two-pass warp kernels)",
+        "roofline": {"bound": "hbm", "kernel": "k_merge (warp-specialised row merge: staged gathers, sort, "
+                                               "look-back, write C)",
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": profile_traffic(args.config, 1),
                      "algorithmic_bytes": ba, "kernel_ms": round(num_ms, 4),
@@ -515,12 +515,12 @@ def ours_multi(args):
     if rank == 0:
         peak, peak_kind = measured_peaks()
         gflops = 2.0 * products_total / (ms * 1e-3) / 1e9
-        num = kt.get("spgemm_tile", kt.get("spgemm_numeric", (1, 0.0)))
+        num = kt.get("spgemm_merge", (1, 0.0))
         kms = num[1] / max(1, num[0])
         # rank 0's multiply: A tile rows/nnz, gathers of its products, its C tile
         ba0 = alg_bytes(int(at.nrows), int(at.nnz) * grid.q, prod0, nnz_c)
         ach = ba0 / (kms * 1e-3) / 1e9 if kms > 0 else None
-        roof0 = {"bound": "hbm", "kernel": "k_tile (rank 0, its trident rounds)", "peak": peak, "unit": "GB/s",
+        roof0 = {"bound": "hbm", "kernel": "k_merge (rank 0, its trident rounds)", "peak": peak, "unit": "GB/s",
                  "achieved": round(ach, 1) if ach else None, "frac": round(ach / peak, 4) if ach else None,
                  "traffic": None, "algorithmic_bytes": ba0, "kernel_ms": round(kms, 4), "products_rank0": prod0,
                  "peak_kind": peak_kind}
