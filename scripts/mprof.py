@@ -29,18 +29,19 @@ print(f"n={n} d={d} nnzC={c.nnz} wall={1e3 * (time.perf_counter() - t0):.2f} ms"
 for k, (cnt, ms) in sorted(dev.timing_read().items()):
     print(f"   {k:22s} {ms / max(cnt, 1):8.3f} ms")
 f(buf)
-names = ["w:wait-ready", "w:claim+gather", "w:cp-wait", "w:sort", "w:rows", "s:wait-freed", "s:stage", "s:tiles",
+names = ["c:wait-next", "c:pre", "c:cp-wait", "c:sort", "c:tiles", "s:wait-freed", "s:stage", "s:tiles",
          "e:wait-ready+done", "e:look-back", "e:rest", "e:tiles"]
 for i, nm in enumerate(names):
     print(f"   {nm:20s} {buf[i]:16d}")
-print(f"   lb:windows {buf[24]}  lb:spins {buf[25]}")
+print(f"   lb:windows {buf[24]}  sum n {buf[25]}  overflow products: total {buf[26]} max n {buf[27]}")
 rows0 = buf[4] or 1
-print(f"   worker per row: claim={buf[1] / rows0:.0f} gather={buf[13] / rows0:.0f} post-sort={buf[14] / rows0:.0f} "
-      f"wait-ready={buf[0] / rows0:.0f} cp-wait={buf[2] / rows0:.0f} sort={buf[3] / rows0:.0f}")
-sp = [buf[16 + i] for i in range(5)]
+print(f"   compute per tile (cycles, summed over compute warps / tiles): pre={buf[1] / rows0:.0f} "
+      f"gather-issue={buf[13] / rows0:.0f} cp-wait={buf[2] / rows0:.0f} sort={buf[3] / rows0:.0f} "
+      f"wait-next={buf[0] / rows0:.0f}")
+sp = [buf[16 + i] for i in range(6)]
 rows = buf[4] or 1
-print("   sort phases (cycles/row): " + " ".join(f"{nm}={v / rows:.0f}" for nm, v in
-                                               zip(["load", "count", "scan", "place", "fix"], sp)))
+print("   sort phases (cycles/tile-warp): " + " ".join(f"{nm}={v / rows:.0f}" for nm, v in
+                                               zip(["P1", "P2+P3", "P5", "compact-count", "compact-write", "P4"], sp)))
 w = sum(buf[i] for i in (0, 1, 2, 3)) or 1
 print("   worker split: " + " ".join(f"{names[i]}={100 * buf[i] / w:.1f}%" for i in (0, 1, 2, 3)))
 e = sum(buf[i] for i in (8, 9, 10)) or 1

@@ -160,6 +160,86 @@ def config(k):
     print(f"config{k}: nnz={d['nnz']} ref {secs:.1f}s")
 
 
+def _views(h):
+    """rowptr/colind/values of a reference matrix handle as numpy views (no copy)."""
+    import ctypes as C
+    L = O._R()
+    nr, nc, nz = C.c_int64(), C.c_int64(), C.c_int64()
+    L.ref_csr_info(h.ptr, C.byref(nr), C.byref(nc), C.byref(nz))
+    nr, nc, nz = nr.value, nc.value, nz.value
+    rp = np.ctypeslib.as_array(L.ref_csr_rowptr(h.ptr), shape=(nr + 1,))
+    ci = np.ctypeslib.as_array(L.ref_csr_colind(h.ptr), shape=(nz,)) if nz else np.zeros(0, np.int64)
+    va = np.ctypeslib.as_array(L.ref_csr_values(h.ptr), shape=(nz,)) if nz else np.zeros(0, np.float64)
+    return nr, nc, nz, rp, ci, va
+
+
+def config3():
+    """Config 3 (R-MAT Graph500, edge factor 16, (a,b,c)=(0.57,0.19,0.19),
+    SplitMix64 draw order of SURVEY.md §8(d), duplicates summed by
+    from_triplets, symmetric random permutation): at scale 18 the digest of
+    the full C = A*A from the reference's spgemm_local (csr.cpp:132-165); at
+    scale 22 (full C ~7.2e10 entries: no host holds it) the reference rows of
+    C for the heaviest row of A*A and 50 random rows with products, each
+    computed as spgemm_local(A[rows, :], A) — exact, since a row of C depends
+    only on its row of A."""
+    import ctypes as C
+    import paper_2603_21444_b200 as spg  # host generator (bit-identical to the reference's from_triplets rules)
+    out = {}
+    # ---- scale 18, full product
+    t0 = time.time()
+    a = spg.gen_rmat(18, 16, 1, 2)
+    ha = O.RefHandle.from_csr(a)
+    gen_s = time.time() - t0
+    secs, nz, o = C.c_double(), C.c_int64(), C.c_void_p()
+    O._chk(O._R().ref_spgemm_local_timed(ha.ptr, ha.ptr, C.byref(secs), C.byref(nz), C.byref(o)))
+    hc = O.RefHandle(o.value)
+    nr, nc, nnz, rp, ci, va = _views(hc)
+    rng = np.random.default_rng(12345)
+    rows = np.sort(rng.choice(nr, size=256, replace=False))
+    samples = {int(i): {"cols": ci[rp[i]:rp[i + 1]].tolist(), "vals": va[rp[i]:rp[i + 1]].tolist()}
+               for i in rows if rp[i + 1] - rp[i] <= 4096}
+    out["s18"] = {"nrows": int(nr), "ncols": int(nc), "nnz": int(nnz), "nnz_A": int(a.nnz),
+                  "products": int(O.port_products(a, a)), "sha_rowptr": sha(rp), "sha_colind": sha(ci),
+                  "sha_values": sha(va), "ref_seconds_1core": secs.value, "gen_seconds": gen_s,
+                  "sample_rows": samples,
+                  "desc": "gen_rmat(18, 16, seed 1, perm seed 2); C = A*A; reference spgemm_local"}
+    print(f"config3 s18: nnz(A)={a.nnz} nnz(C)={nnz} ref {secs.value:.1f}s")
+    del hc, ha, a, ci, va, rp
+    # ---- scale 22, sampled rows
+    a = spg.gen_rmat(22, 16, 1, 2)
+    _, prod = O.port_products(a, a, per_row=True)
+    heavy = int(np.argmax(prod))
+    rng = np.random.default_rng(22)
+    cand = np.nonzero(prod > 0)[0]
+    rows = np.unique(np.concatenate([[heavy], rng.choice(cand, size=50, replace=False)]))
+    rp = np.asarray(a.rowptr)
+    sub_rp = [0]
+    sub_ci, sub_va = [], []
+    for i in rows:
+        sub_ci.append(np.asarray(a.colind[rp[i]:rp[i + 1]], np.int64))
+        sub_va.append(np.asarray(a.values[rp[i]:rp[i + 1]], np.float64))
+        sub_rp.append(sub_rp[-1] + rp[i + 1] - rp[i])
+    sub = O.Csr(len(rows), a.ncols, np.array(sub_rp, np.int64), np.concatenate(sub_ci), np.concatenate(sub_va))
+    t0 = time.time()
+    cs = O.ref_spgemm_local(sub, a)
+    secs22 = time.time() - t0
+    srows = {}
+    for t, i in enumerate(rows):
+        lo, hi = int(cs.rowptr[t]), int(cs.rowptr[t + 1])
+        cols, vals = np.asarray(cs.colind[lo:hi], np.int64), np.asarray(cs.values[lo:hi], np.float64)
+        e = {"products": int(prod[i]), "nnz": hi - lo, "sha_cols": sha(cols), "sha_vals": sha(vals)}
+        if hi - lo <= 4096:
+            e["cols"], e["vals"] = cols.tolist(), vals.tolist()
+        srows[int(i)] = e
+    out["s22"] = {"nrows": int(a.nrows), "nnz_A": int(a.nnz), "products_total": int(prod.sum()),
+                  "heaviest_row": heavy, "ref_seconds_rows": secs22, "rows": srows,
+                  "desc": "gen_rmat(22, 16, seed 1, perm seed 2); rows of C = A*A by spgemm_local(A[rows,:], A)"}
+    print(f"config3 s22: heaviest row {heavy} products {int(prod[heavy])} nnz {srows[heavy]['nnz']}; "
+          f"{len(rows)} rows in {secs22:.1f}s")
+    with open(os.path.join(HERE, "config3.json"), "w") as f:
+        json.dump(out, f)
+
+
 def mcl4():
     """Adds to config4.json the digest of one MCL post-step of config 4's
     product with the reference's own functions (apps.cpp:79-82: normalize,
@@ -189,5 +269,7 @@ if __name__ == "__main__":
             config(k)
     if what == "mcl4":
         mcl4()
-    if what.startswith("config") and what != "configs":
+    if what == "config3":
+        config3()
+    elif what.startswith("config") and what != "configs":
         config(int(what[6:]))
