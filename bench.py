@@ -41,6 +41,7 @@ CONFIGS = {
     2: dict(n=1 << 22, d=16.0, desc="Erdos-Renyi n=2^22, 16 nnz/row, C=A*A fp64"),
     4: dict(n=1 << 21, d=16.0, desc="MCL expansion: column_normalize(ER 2^21, 16/row) squared", mcl=True),
 }
+NVLINK_GBS = 900.0  # NVLink 5 per direction per GPU (B200)
 METRIC = "SpGEMM GFLOP/s and ms per C=A·B at 1/2/4/8 B200; % HBM roofline"
 
 
@@ -112,12 +113,23 @@ def make_input(cfg):
     return a
 
 
+def kernel_source_sha():
+    import hashlib
+    with open(os.path.join(ROOT, "paper_2603_21444_b200", "csrc", "spgemm.cu"), "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()[:16]
+
+
 def profile_traffic(cfg, world):
-    """dram bytes per launch of the numeric kernel from the committed ncu capture."""
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the numeric
+    kernel from the committed `ncu --set full` capture (profiles/traffic.json,
+    written by scripts/ncu_traffic.py). Used only when the capture was taken
+    of the kernel source being benchmarked (sha256 of spgemm.cu), else null."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return d.get(f"config{cfg}_n{world}")
+        e = d.get(f"config{cfg}_n{world}")
+        if isinstance(e, dict) and e.get("spgemm_cu_sha16") == kernel_source_sha():
+            return e.get("bytes")
     return None
 
 
@@ -271,7 +283,7 @@ def ours_single(args):
     kt = dev.timing_read()
     own = {k: v for k, v in kt.items()}
     launches = sum(v[0] for v in own.values())
-    kname = "spgemm_merge"
+    kname = "spgemm_tile"
     num_ms = own.get(kname, (1, 0.0))[1] / max(1, own.get(kname, (1, 0))[0])
     dev.timing(False)
 
@@ -314,7 +326,7 @@ def ours_single(args):
         dev.synchronize()
         return (time.perf_counter() - t0) / e2e_steps * 1e3
 
-    e2e_steps = max(1, min(args.steps, int(os.environ.get("SPG_E2E_STEPS", 3))))
+    e2e_steps = max(1, int(os.environ.get("SPG_E2E_STEPS", args.steps)))
     e2e_ms_two = e2e_time(e2e_two_calls)
     ref_rp, ref_ci, ref_va = c_rp.copy(), c_ci[::1009].copy(), c_va[::1009].copy()
     c_rp[:] = -1
@@ -341,7 +353,7 @@ def ours_single(args):
         "config": {"workload": CONFIGS[args.config]["desc"], "config_id": args.config, "grid": "P=1 lambda=1 q=1",
                    "products": products, "nnz_A": nnz_a, "nnz_C": nnz_c,
                    "l2": "inputs (1.6 GB) and C (12.9 GB) larger than the 126 MB L2; no flush"},
-        "roofline": {"bound": "hbm", "kernel": "k_merge (warp-specialised row merge: staged gathers, sort, "
+        "roofline": {"bound": "hbm", "kernel": "k_tile (single-pass tile multiply: gathers, bucket sort, "
                                                "look-back, write C)",
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": profile_traffic(args.config, 1),
@@ -479,9 +491,12 @@ def ours_multi(args):
         t2 = time.perf_counter()
         _capi.check(L.spg_csr_download(dev.ctx, c.h, c_rp.ctypes.data, c_ci.ctypes.data, 4, c_va.ctypes.data))
         c.free()
+        # every peer's pulls of this rank's tiles are done before the next
+        # reload overwrites them (RankExchange.reload contract)
+        dist.barrier()
         phase[:] += (t1 - t0, t2 - t1, time.perf_counter() - t2)
 
-    e2e_steps = max(1, min(args.steps, int(os.environ.get("SPG_E2E_STEPS", 3))))
+    e2e_steps = max(1, int(os.environ.get("SPG_E2E_STEPS", args.steps)))
     e2e_step()
     dist.barrier()
     t0 = time.perf_counter()
@@ -515,12 +530,12 @@ def ours_multi(args):
     if rank == 0:
         peak, peak_kind = measured_peaks()
         gflops = 2.0 * products_total / (ms * 1e-3) / 1e9
-        num = kt.get("spgemm_merge", (1, 0.0))
+        num = kt.get("spgemm_tile", (1, 0.0))
         kms = num[1] / max(1, num[0])
         # rank 0's multiply: A tile rows/nnz, gathers of its products, its C tile
         ba0 = alg_bytes(int(at.nrows), int(at.nnz) * grid.q, prod0, nnz_c)
         ach = ba0 / (kms * 1e-3) / 1e9 if kms > 0 else None
-        roof0 = {"bound": "hbm", "kernel": "k_merge (rank 0, its trident rounds)", "peak": peak, "unit": "GB/s",
+        roof0 = {"bound": "hbm", "kernel": "k_tile (rank 0, its trident rounds)", "peak": peak, "unit": "GB/s",
                  "achieved": round(ach, 1) if ach else None, "frac": round(ach / peak, 4) if ach else None,
                  "traffic": None, "algorithmic_bytes": ba0, "kernel_ms": round(kms, 4), "products_rank0": prod0,
                  "peak_kind": peak_kind}
@@ -534,8 +549,8 @@ def ours_multi(args):
                        "l2": "inputs and C larger than L2; no flush"},
             "kernel_ms_rank0": {k: round(v[1] / max(1, v[0]), 4) for k, v in kt.items()},
             "exchange": {"ledger_max_recv_bytes_per_rank": recv_bytes, "exchange_ms_rank0": round(exch_ms, 4),
-                         "nvlink_frac_rank0": round(recv_bytes / max(exch_ms, 1e-9) / 1e6 / 770.0, 4),
-                         "nvlink_peak_gbs": 770.0},
+                         "nvlink_frac_rank0": round(recv_bytes / max(exch_ms, 1e-9) / 1e6 / NVLINK_GBS, 4),
+                         "nvlink_peak_gbs": NVLINK_GBS},
             "roofline": roof0,
             "e2e": {"value": round(2.0 * products_total / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
                     "ms_per_step": round(e2e_ms, 2), "h2d_bytes_per_step": int(hb[0].item()),

@@ -215,12 +215,53 @@ spg_status spg_trident_spgemm(spg_ctx* const* ctxs, int nctx, const spg_csr* con
                               int value_width, spg_csr** c_tiles_out, spg_ledger_cell* ledger_out,
                               double* timeline_out);
 
+/* One exchange timeline event, mirrors TimelineEvent (engine.hpp:25-38).
+ * type: 0 enqueue-request, 1 serve-request, 2 transfer-complete,
+ * 3 allgather-complete, 4 compute-complete (EventType, engine.hpp:15-21);
+ * operand: 0 A, 1 B; link: 0 SELF, 1 LI, 2 GI (LinkClass, netmodel.hpp:11).
+ * src/dst/round/operand/link/nnz/bytes follow the reference engine's
+ * bookkeeping (engine.cpp:228-302); t_start/t_end are MEASURED seconds from the
+ * rank's start (CUDA events on its device), not the modeled alpha-beta clock.
+ * allgather-complete: src = node id, dst = -1, times over the node's members. */
+typedef struct spg_event {
+    int32_t type, src, dst, round, operand, link;
+    double t_start, t_end;
+    int64_t nnz, bytes;
+} spg_event;
+
+/* spg_trident_spgemm with the measured exchange record. The ledger is built
+ * from the tiles each rank actually consumed (one log entry per pull or
+ * in-place read of another rank's tile, with its rows and nnz), booked along
+ * the reference's routes: A and the rank's own B slice index from their
+ * owners (GI/LI by node), the other slices of B_{s,j} as the node's LI
+ * allgather (engine.cpp:228-302). node_start_delay (optional, n_delays
+ * entries, seconds): virtual node n's ranks start their pulls after that delay
+ * on the device (the reference's skew knob, engine.cpp:217-221).
+ * events_out (optional): up to events_cap events; *n_events (optional)
+ * receives how many were produced (SPG_PARAMETER_ERROR if more than events_cap;
+ * C, ledger and timeline are still complete then).
+ * xfer_out (optional): P*4 doubles per rank [device bytes pulled, pull ms
+ * (first pull start to last pull end), tiles pulled, tiles read in place]. */
+spg_status spg_trident_spgemm_ex(spg_ctx* const* ctxs, int nctx, const spg_csr* const* a_tiles,
+                                 const spg_csr* const* b_tiles, int procs, int gpus_per_node, int index_width,
+                                 int value_width, const double* node_start_delay, int n_delays,
+                                 spg_csr** c_tiles_out, spg_ledger_cell* ledger_out, double* timeline_out,
+                                 spg_event* events_out, int events_cap, int* n_events, double* xfer_out);
+
 /* Single-process Sparse SUMMA (algorithms.cpp:103-174) on a sqrt(P) x sqrt(P)
  * grid2d partition; ledger as above (node_of = rank / gpus_per_node). */
 spg_status spg_summa_spgemm(spg_ctx* const* ctxs, int nctx, const spg_csr* const* a_tiles,
                             const spg_csr* const* b_tiles, int procs, int gpus_per_node, int index_width,
                             int value_width, spg_csr** c_tiles_out, spg_ledger_cell* ledger_out,
                             double* timeline_out);
+/* spg_summa_spgemm with the measured exchange record (events as the
+ * reference's summa_spgemm emits them: transfer-complete per remote tile,
+ * compute-complete per rank and round; algorithms.cpp:133-166). */
+spg_status spg_summa_spgemm_ex(spg_ctx* const* ctxs, int nctx, const spg_csr* const* a_tiles,
+                               const spg_csr* const* b_tiles, int procs, int gpus_per_node, int index_width,
+                               int value_width, spg_csr** c_tiles_out, spg_ledger_cell* ledger_out,
+                               double* timeline_out, spg_event* events_out, int events_cap, int* n_events,
+                               double* xfer_out);
 
 /* Single-process sparsity-aware 1D driver (algorithms.cpp:176-269) on a
  * rows1d partition of A and B (tile r on ctxs[r % nctx]). Rank p pulls exactly

@@ -294,6 +294,22 @@ def ref_run_algo(algo: str, a, b, procs: int, gpus_per_node: int, want_c: bool =
             "makespan": ms.value, "events": ev}
 
 
+def ref_timeline_jsonl(algo: str, a, b, procs: int, gpus_per_node: int, node_start_delay=None) -> str:
+    """The reference's dr.timeline.to_jsonl() (engine.cpp:25-41) of run_algo."""
+    ha, hb = _h(a), _h(b)
+    d = np.asarray(node_start_delay if node_start_delay is not None else [], np.float64)
+    n = C.c_size_t()
+    L = _R()
+    L.ref_timeline_jsonl.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int,
+                                     C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]
+    _chk(L.ref_timeline_jsonl(ALGOS[algo], ha.ptr, hb.ptr, procs, gpus_per_node, d.ctypes.data, len(d), None, 0,
+                              C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _chk(L.ref_timeline_jsonl(ALGOS[algo], ha.ptr, hb.ptr, procs, gpus_per_node, d.ctypes.data, len(d), buf,
+                              n.value + 1, C.byref(n)))
+    return buf.value.decode()
+
+
 def ref_grid_q(procs: int, gpus_per_node: int) -> int:
     q = C.c_int()
     _chk(_R().ref_grid(procs, gpus_per_node, C.byref(q)))

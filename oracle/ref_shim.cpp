@@ -236,6 +236,31 @@ int ref_run_algo(int algo, const void* a, const void* b, int procs, int gpus_per
     });
 }
 
+// The reference's own dr.timeline.to_jsonl() (engine.cpp:25-41) of run_algo
+// (node_start_delay optional, trident only: n_delays entries) into buf (cap
+// bytes, NUL-terminated when it fits); *len receives the full length.
+int ref_timeline_jsonl(int algo, const void* a, const void* b, int procs, int gpus_per_node, const double* delays,
+                       int n_delays, char* buf, std::size_t cap, std::size_t* len) {
+    return guarded([&] {
+        const TopologySpec topo = TopologySpec::preset(0, gpus_per_node);
+        const CsrMatrix& A = *static_cast<const CsrMatrix*>(a);
+        const CsrMatrix& B = *static_cast<const CsrMatrix*>(b);
+        DriverResult dr;
+        if (algo == 0 && n_delays > 0)
+            dr = trident_spgemm(A, B, TridentGrid::create(procs, gpus_per_node), topo,
+                                std::vector<double>(delays, delays + n_delays));
+        else
+            dr = run_algo(algo == 0 ? Algo::trident : algo == 1 ? Algo::summa : Algo::oned, A, B, procs,
+                          gpus_per_node, topo);
+        const std::string j = dr.timeline.to_jsonl();
+        *len = j.size();
+        if (buf && cap > j.size()) {
+            std::memcpy(buf, j.data(), j.size());
+            buf[j.size()] = 0;
+        }
+    });
+}
+
 int ref_grid(int procs, int gpus_per_node, int* q) {
     return guarded([&] { *q = TridentGrid::create(procs, gpus_per_node).q; });
 }

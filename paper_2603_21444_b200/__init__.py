@@ -10,6 +10,7 @@ library or no device the calls raise — there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes as C
+import json
 import math
 import os
 from dataclasses import dataclass, field
@@ -664,10 +665,18 @@ def trident_ledger(grid: TridentGrid, a_shapes, b_shapes, iw: int = 4, vw: int =
     return L
 
 
+EVENT_NAMES = ("enqueue-request", "serve-request", "transfer-complete", "allgather-complete", "compute-complete")
+LINK_NAMES = ("SELF", "LI", "GI")
+
+
 @dataclass
 class DriverResult:
-    """algorithms.hpp:32-38; ledger as the uint64 array of trident_ledger;
-    timeline: (procs, rounds, 4) ms [exchange, exposed wait, multiply, merge]."""
+    """algorithms.hpp:32-38; ledger as the uint64 array of trident_ledger,
+    built from the tiles the ranks actually consumed; timeline: (procs,
+    rounds, 4) ms [exchange, exposed wait, multiply, merge]; events: the
+    measured TimelineEvents (engine.hpp:25-38) as dicts, times in seconds from
+    each rank's start; xfer: (procs, 4) [device bytes pulled, pull span ms,
+    tiles pulled, tiles of other ranks read in place]."""
 
     c: CsrMatrix
     ledger: np.ndarray
@@ -675,6 +684,19 @@ class DriverResult:
     makespan: float
     rounds: int
     checksum: tuple | None = None  # (nnz, hash) of C, result_checksum computed on the device
+    events: list = field(default_factory=list)
+    xfer: np.ndarray | None = None
+
+    def to_jsonl(self) -> str:
+        """EventTimeline::to_jsonl (engine.cpp:25-41): one JSON object per
+        event, keys in the reference's order."""
+        out = []
+        for e in self.events:
+            out.append(json.dumps({"type": e["type"], "actors": [e["src"], e["dst"]], "round": e["round"],
+                                   "t_start": e["t_start"], "t_end": e["t_end"], "bytes": e["bytes"],
+                                   "operand": e["operand"], "link": e["link"], "nnz": e["nnz"]},
+                                  separators=(",", ":")))
+        return "".join(x + "\n" for x in out)
 
 
 def _devices_for(procs: int):
@@ -684,10 +706,11 @@ def _devices_for(procs: int):
     return [default_device(d) for d in range(min(n, procs))]
 
 
-def _run_driver(fn, a, b, procs, lam, scheme, cmap, rounds, topo) -> DriverResult:
+def _run_driver(fn, a, b, procs, lam, scheme, cmap, rounds, topo, delays=None) -> DriverResult:
     """Device tile store end to end: ONE upload of each global operand, the
     tiles split on the GPUs (spg_partition), the driver, the C tiles merged on
-    device 0 (spg_reassemble) and ONE download of C."""
+    device 0 (spg_reassemble) and ONE download of C. fn: the _ex driver
+    (measured ledger + events) for trident / summa, spg_oned_spgemm else."""
     devs = _devices_for(procs)
     nctx = len(devs)
     plam = lam if scheme == "trident" else 1
@@ -702,7 +725,28 @@ def _run_driver(fn, a, b, procs, lam, scheme, cmap, rounds, topo) -> DriverResul
     hc = (C.c_void_p * procs)()
     cells = (_capi.LedgerCell * (procs * 4))()
     tl = (C.c_double * (procs * rounds * 4))()
-    check(fn(ctxs, nctx, ha, hb, procs, lam, topo.index_width, topo.value_width, hc, cells, tl))
+    L = _capi.lib()
+    events, xfer = [], None
+    if fn in (L.spg_trident_spgemm_ex, L.spg_summa_spgemm_ex):
+        cap = procs * rounds * 8 + 16
+        ev = (_capi.Event * cap)()
+        nev = C.c_int()
+        xf = (C.c_double * (procs * 4))()
+        if fn == L.spg_trident_spgemm_ex:
+            d = np.asarray(delays if delays is not None else [], np.float64)
+            dp = d.ctypes.data_as(C.POINTER(C.c_double)) if len(d) else None
+            check(fn(ctxs, nctx, ha, hb, procs, lam, topo.index_width, topo.value_width, dp, len(d), hc, cells, tl,
+                     ev, cap, C.byref(nev), xf))
+        else:
+            check(fn(ctxs, nctx, ha, hb, procs, lam, topo.index_width, topo.value_width, hc, cells, tl, ev, cap,
+                     C.byref(nev), xf))
+        for x in ev[:nev.value]:
+            events.append({"type": EVENT_NAMES[x.type], "src": x.src, "dst": x.dst, "round": x.round,
+                           "operand": "AB"[x.operand], "link": LINK_NAMES[x.link], "t_start": x.t_start,
+                           "t_end": x.t_end, "nnz": x.nnz, "bytes": x.bytes})
+        xfer = np.ctypeslib.as_array(xf).reshape(procs, 4).copy()
+    else:
+        check(fn(ctxs, nctx, ha, hb, procs, lam, topo.index_width, topo.value_width, hc, cells, tl))
     dc = [DeviceCsr(devs[r % nctx], hc[r]) for r in range(procs)]
     gc = devs[0].reassemble(dc, cmap)
     cs = gc.checksum()
@@ -710,17 +754,22 @@ def _run_driver(fn, a, b, procs, lam, scheme, cmap, rounds, topo) -> DriverResul
     led = np.array([[x.messages, x.nnz, x.bytes] for x in cells], np.uint64).reshape(procs, 2, 2, 3)
     tla = np.ctypeslib.as_array(tl).reshape(procs, rounds, 4).copy()
     makespan = float((tla[:, :, 1:].sum(axis=(1, 2))).max()) * 1e-3
-    return DriverResult(c, led, tla, makespan, rounds, cs)
+    return DriverResult(c, led, tla, makespan, rounds, cs, events, xfer)
 
 
-def trident_spgemm(a, b, grid: TridentGrid, topo: TopologySpec | None = None) -> DriverResult:
-    """algorithms.cpp:24-101 on the GPUs of this box (rank r -> device r % ndev)."""
+def trident_spgemm(a, b, grid: TridentGrid, topo: TopologySpec | None = None,
+                   node_start_delay=None) -> DriverResult:
+    """algorithms.cpp:24-101 on the GPUs of this box (rank r -> device r % ndev).
+    node_start_delay: seconds per virtual node; that node's ranks start their
+    pulls that much later on the device (engine.cpp:217-221)."""
     if int(a.ncols) != int(b.nrows):
         raise SpgError(2, f"trident_spgemm: a.ncols={a.ncols} != b.nrows={b.nrows}")
     topo = topo or TopologySpec(grid.gpus_per_node)
     cmap = make_tile_map(int(a.nrows), int(b.ncols), "trident", grid.procs, grid.gpus_per_node)
-    return _run_driver(_capi.lib().spg_trident_spgemm, a, b, grid.procs, grid.gpus_per_node, "trident", cmap, grid.q,
-                       topo)
+    if node_start_delay is not None and any(not (float(x) >= 0.0) for x in node_start_delay):
+        raise SpgError(3, "trident_spgemm: node_start_delay must be >= 0")
+    return _run_driver(_capi.lib().spg_trident_spgemm_ex, a, b, grid.procs, grid.gpus_per_node, "trident", cmap,
+                       grid.q, topo, node_start_delay)
 
 
 def summa_spgemm(a, b, procs: int, gpus_per_node: int, topo: TopologySpec | None = None) -> DriverResult:
@@ -732,7 +781,7 @@ def summa_spgemm(a, b, procs: int, gpus_per_node: int, topo: TopologySpec | None
         raise SpgError(4, f"summa: P={procs} is not a perfect square")
     topo = topo or TopologySpec(gpus_per_node)
     cmap = make_tile_map(int(a.nrows), int(b.ncols), "grid2d", procs, 1)
-    return _run_driver(_capi.lib().spg_summa_spgemm, a, b, procs, gpus_per_node, "grid2d", cmap, pr, topo)
+    return _run_driver(_capi.lib().spg_summa_spgemm_ex, a, b, procs, gpus_per_node, "grid2d", cmap, pr, topo)
 
 
 def oned_spgemm(a, b, procs: int, gpus_per_node: int, topo: TopologySpec | None = None) -> DriverResult:

@@ -21,6 +21,7 @@ EXPORTS = [
     "spg_csr_device_ptrs", "spg_spgemm", "spg_spgemm_products", "spg_spgeam", "spg_spgeam_inplace",
     "spg_vconcat", "spg_csr_extract", "spg_csr_copy", "spg_tile_rects", "spg_partition", "spg_reassemble", "spg_spgemm_host", "spg_spgemm_host_to_host", "spg_column_normalize", "spg_prune", "spg_elementwise_power", "spg_mcl_poststep",
     "spg_trident_grid", "spg_trident_spgemm", "spg_summa_spgemm", "spg_oned_spgemm",
+    "spg_trident_spgemm_ex", "spg_summa_spgemm_ex",
     "spg_host_register", "spg_host_unregister",
     "spg_csr_ipc_export", "spg_csr_ipc_open", "spg_csr_make_shareable", "spg_trident_rank",
 ]
@@ -36,6 +37,13 @@ IPC_BYTES = 256
 
 class LedgerCell(C.Structure):
     _fields_ = [("messages", C.c_uint64), ("nnz", C.c_uint64), ("bytes", C.c_uint64)]
+
+
+class Event(C.Structure):
+    """spg_event (capi.h): one measured TimelineEvent (engine.hpp:25-38)."""
+    _fields_ = [("type", C.c_int32), ("src", C.c_int32), ("dst", C.c_int32), ("round", C.c_int32),
+                ("operand", C.c_int32), ("link", C.c_int32), ("t_start", C.c_double), ("t_end", C.c_double),
+                ("nnz", C.c_int64), ("bytes", C.c_int64)]
 
 
 _lib = None
@@ -92,6 +100,10 @@ def lib() -> C.CDLL:
         "spg_trident_spgemm": (st, [P(vp), i32, P(vp), P(vp), i32, i32, i32, i32, P(vp), P(LedgerCell), P(f64)]),
         "spg_oned_spgemm": (st, [P(vp), i32, P(vp), P(vp), i32, i32, i32, i32, P(vp), P(LedgerCell), P(f64)]),
         "spg_summa_spgemm": (st, [P(vp), i32, P(vp), P(vp), i32, i32, i32, i32, P(vp), P(LedgerCell), P(f64)]),
+        "spg_trident_spgemm_ex": (st, [P(vp), i32, P(vp), P(vp), i32, i32, i32, i32, P(f64), i32, P(vp),
+                                       P(LedgerCell), P(f64), P(Event), i32, P(i32), P(f64)]),
+        "spg_summa_spgemm_ex": (st, [P(vp), i32, P(vp), P(vp), i32, i32, i32, i32, P(vp), P(LedgerCell), P(f64),
+                                     P(Event), i32, P(i32), P(f64)]),
         "spg_host_register": (st, [vp, C.c_size_t]),
         "spg_host_unregister": (st, [vp]),
         "spg_csr_ipc_export": (st, [vp, C.c_char_p]),

@@ -117,8 +117,6 @@ spg_status spg_init(int device, spg_ctx** out) {
         ctx->l2_bytes = prop.l2CacheSize;
         ctx->mem_total = prop.totalGlobalMem;
         ctx_live(device, 1);
-        const char* tp = std::getenv("SPG_TWO_PASS");
-        ctx->two_pass = (tp && tp[0] == '1') ? 1 : 0;
         SPG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         for (int i = 0; i < spg_ctx::NAUX; ++i) SPG_CUDA(cudaStreamCreateWithFlags(&ctx->aux[i], cudaStreamNonBlocking));
         SPG_CUDA(cudaStreamCreateWithFlags(&ctx->xfer, cudaStreamNonBlocking));

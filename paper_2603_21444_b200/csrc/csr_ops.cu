@@ -612,7 +612,8 @@ spg_csr* copy_csr(spg_ctx* ctx, const spg_csr* s) {
     return c;
 }
 
-spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n, cudaEvent_t rp_ready) {
+spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n, cudaEvent_t rp_ready,
+                 std::vector<SlicePull>* log) {
     if (n == 0) {
         spg_csr* z = new_csr(ctx, 0, 0, 0);
         if (rp_ready) SPG_CUDA(cudaEventRecord(rp_ready, ctx->stream));
@@ -630,10 +631,20 @@ spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n, cudaEvent_t 
     if (n > 1 && ctx->aux[0]) SPG_CUDA(cudaEventRecord(ctx->aux_ev[spg_ctx::NAUX], ctx->stream));  // fork point
     int64_t r = 0, base = 0;
     const int dd = ctx->device;
+    if (log) log->assign(n, SlicePull{});
     for (int s = 0; s < n; ++s) {
         const spg_csr* sl = slices[s];
         const int sd = sl->ctx->device;
         const int64_t* rp = sl->rowptr;
+        if (log) {
+            SlicePull& L = (*log)[s];
+            L.rows = sl->nrows;
+            L.nnz = sl->nnz;
+            L.dev_bytes = (sl->nrows + 1) * int64_t(sizeof(int64_t)) + sl->nnz * int64_t(sizeof(int32_t) + sizeof(double));
+            L.t0 = ctx->timer.ev();
+            L.t1 = ctx->timer.ev();
+            SPG_CUDA(cudaEventRecord(L.t0, ctx->stream));
+        }
         DBuf<int64_t> tmp(ctx, sd == dd ? 0 : sl->nrows + 1);
         if (sd != dd) {
             SPG_CUDA(cudaMemcpyPeerAsync(tmp.get(), dd, sl->rowptr, sd, (sl->nrows + 1) * sizeof(int64_t), ctx->stream));
@@ -659,6 +670,9 @@ spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n, cudaEvent_t 
                 SPG_CUDA(cudaMemcpyPeerAsync(out->colind + base, dd, sl->colind, sd, sl->nnz * sizeof(int32_t), st));
                 SPG_CUDA(cudaMemcpyPeerAsync(out->values + base, dd, sl->values, sd, sl->nnz * sizeof(double), st));
             }
+            if (log) SPG_CUDA(cudaEventRecord((*log)[s].t1, st));
+        } else if (log) {
+            SPG_CUDA(cudaEventRecord((*log)[s].t1, ctx->stream));
         }
         r += sl->nrows;
         base += sl->nnz;

@@ -77,7 +77,6 @@ struct spg_ctx {
     // multi-GB request maps fresh memory on every call (see big_alloc).
     std::vector<std::pair<void*, size_t>> big_cache;
     size_t mem_total = 0;  // device memory (sizes the block cache)
-    int two_pass = 0;  // 1: symbolic + numeric warp kernels instead of the single-pass tiles (SPG_TWO_PASS=1)
 };
 
 struct spg_csr {
@@ -185,7 +184,14 @@ int64_t spgemm_products(spg_ctx* ctx, const spg_csr* a, const spg_csr* b);
 spg_csr* spgeam(spg_ctx* ctx, const spg_csr* a, const spg_csr* b);
 // rp_ready (optional): recorded once the row pointers are assembled; the
 // column/value pulls may still be running on the aux streams then.
-spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n, cudaEvent_t rp_ready = nullptr);
+// One slice pull of vconcat, for the exchange log: t0/t1 bracket its copies
+// on the stream that ran them (pooled events of ctx->timer).
+struct SlicePull {
+    int64_t rows = 0, nnz = 0, dev_bytes = 0;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+};
+spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n, cudaEvent_t rp_ready = nullptr,
+                 std::vector<SlicePull>* log = nullptr);
 // [A_0 | A_1 | ...] of row-aligned parts (at most 16)
 spg_csr* hconcat(spg_ctx* ctx, const spg_csr* const* parts, int n);
 spg_csr* extract(spg_ctx* ctx, const spg_csr* m, int64_t r0, int64_t r1, int64_t c0, int64_t c1);

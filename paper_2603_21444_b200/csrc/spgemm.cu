@@ -3,28 +3,19 @@
 //
 // Row-wise Gustavson in one pass over B:
 //
-//   k_row_plan   per row of A: products, staged slots, tile weight, kind; per
-//                A entry its B row block (espan = block << 32 | length)
+//   k_row_prep   per row of A: products, kind (SMALL / MEDIUM / BIG), tile
+//                weight; per A entry of a tile row its packed span (B row
+//                start, length, product offset in the row, row products)
 //   tiles        runs of consecutive SMALL rows within one TW-window of the
-//                weight prefix (k_tile_flags + scan + k_tile_scatter); every
-//                BIG row is a tile of its own, multiplied by the side path
-//   k_pack_rows  B re-laid as one 128-byte-aligned block per row:
-//                [columns, padded to 4 with -1 | values, padded to 4]
-//   side path    BIG rows (too many slots for a warp row: R-MAT hubs) — ESC
-//   k_merge      persistent, warp-specialised, one CTA per SM:
-//                 * setup warp: takes tile tickets and stages the tile's A
-//                   side (entry spans, A values, row pointers) into shared
-//                   memory with three cp.async.bulk (TMA) copies;
-//                 * 12 row workers: claim rows of the staged tiles; each
-//                   worker gathers its next row's B blocks with 16-byte
-//                   cp.async (half a warp per entry, a B block is contiguous)
-//                   while it sorts the previous one: count into per-row
-//                   column buckets (smem atomics), scan, place, order each
-//                   multi-product bucket by (column, slot), sum duplicate
-//                   columns in slot order = ascending k — the row's C entries
-//                   replace its staged products in place;
-//                 * 2 epilogue warps: decoupled look-back over the tiles'
-//                   nnz for the tile's offset in C, row pointers, copy-out.
+//                weight prefix (k_tile_flags + scan + k_tile_scatter); MEDIUM
+//                and BIG rows are tiles of their own
+//   side path    BIG rows (R-MAT hubs): sort-based ESC, computed before k_tile;
+//                k_big_copy moves them into C after it
+//   k_tile       persistent CTAs, tiles from a global ticket: gather the tile's
+//                products into registers, multiply, bucket by (row, column),
+//                scan, place, rank shared buckets, fold duplicates in
+//                ascending k, decoupled look-back over the tiles' nnz, copy the
+//                tile's C rows out as one contiguous run.
 //
 // Values are bit-identical to the reference: every C entry is
 // 0 + a*b for its first product, then + a*b in ascending k, with separate
@@ -55,157 +46,67 @@ __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a,
 
 constexpr unsigned FULL = 0xffffffffu;
 
-// ------------------------------------------------------------------ geometry
-namespace mg {
-#ifndef SPG_MERGE_NWORK
-#define SPG_MERGE_NWORK 12
+// Monotone map column -> [0, nb): high bits of the column scaled by nb.
+__device__ __forceinline__ int bucket_of(uint32_t col, int cshift, int nb) {
+    return static_cast<int>(__umulhi(col << cshift, static_cast<uint32_t>(nb)));
+}
+
+namespace tile {
+#ifndef SPG_TILE_NT
+#define SPG_TILE_NT 256
 #endif
-#ifndef SPG_MERGE_NST
-#define SPG_MERGE_NST 3
+constexpr int NT = SPG_TILE_NT;                 // threads per CTA
+constexpr int NW = NT / 32;
+constexpr int SMALL_P = 512;                    // a tile row has <= SMALL_P products
+constexpr int SMALL_E = 64;                     // ... and <= SMALL_E entries
+constexpr int ROW_W_MAX = SMALL_P + 4 * SMALL_E + 4;
+#ifndef SPG_TILE_W
+#define SPG_TILE_W 2048
 #endif
-#ifndef SPG_MERGE_TS
-#define SPG_MERGE_TS 2560
+constexpr int TW = SPG_TILE_W;                  // tile window of the row weight prefix
+constexpr int PMAX = TW + ROW_W_MAX;            // bound of products, 4*entries, 4*rows of a tile
+constexpr int EMAX = PMAX / 4;
+constexpr int RMAX = PMAX / 4;
+constexpr int NJ = (PMAX + NT - 1) / NT;        // product slots per thread
+constexpr int EPT = (EMAX + NT - 1) / NT;       // entry slots per thread
+constexpr int HW = PMAX / 32 + 2;               // words of the head bitmap
+constexpr int LMAX = PMAX / 3 + 1;              // shared buckets of >= 3 products
+#ifndef SPG_TILE_BPP
+#define SPG_TILE_BPP 2
 #endif
-constexpr int NWORK = SPG_MERGE_NWORK; // row workers
-constexpr int NEPI = 2;                // epilogue warps
-constexpr int WSETUP = NWORK;          // warp id of the setup warp
-constexpr int WEPI = NWORK + 1;        // first epilogue warp
-constexpr int NWARP = NWORK + 1 + NEPI;
-constexpr int NT = 32 * NWARP;
-constexpr int NST = SPG_MERGE_NST;     // tile stages
-constexpr int TS = SPG_MERGE_TS;       // tile weight capacity: slots <= TS, entries/rows <= TS/8
-constexpr int TE = TS / 8, TR = TS / 8;
-constexpr int RS = 512;                // slots of a worker row
-constexpr int J = RS / 32;             // slots per lane
-constexpr int RW = 640;                // weight of a SMALL row <= RW (so entries <= 79)
-constexpr int TW = TS - RW;            // tiling window
-#ifndef SPG_MERGE_BPS
-#define SPG_MERGE_BPS 2
-#endif
-constexpr int BPS = SPG_MERGE_BPS;     // column buckets per staged slot of a row
-constexpr int CW = BPS * RS + 8;       // bucket words per worker (claim tag << 16 | extra count)
-constexpr int EMIN = 8;                // weight of an entry >= EMIN, of a row >= EMIN
-}  // namespace mg
+constexpr int BPP = SPG_TILE_BPP;               // column buckets per product of a row (2 or 4)
+constexpr int CW = BPP / 2;                     // counter words per product (2 x 16-bit counters a word)
+// espan[e] of an entry of a tile row: B row start (30 bits) | B row length (10)
+// | product offset of the entry in its row (12) | products of the row (12)
+constexpr int SP_BS = 30, SP_LEN = 30, SP_IN = 40, SP_PR = 52;
+constexpr int SP_LEN_MAX = 1023;
+constexpr uint64_t SP_BS_MASK = (uint64_t(1) << SP_BS) - 1;
+}  // namespace tile
 
-// B row block of row k in the packed copy: 128-byte units from the packed base.
-// Disjoint for consecutive rows: start(k+1) - start(k) >= 12*len(k)/128 + 1 units
-// and a block is 12*roundup4(len) <= 12*len + 36 bytes.
-__host__ __device__ __forceinline__ uint64_t block_of(int64_t brow_start, int64_t k) {
-    return static_cast<uint64_t>((12 * brow_start) / 128 + 2 * k);
-}
-__host__ __device__ __forceinline__ int64_t packed_units(int64_t nnz, int64_t nrows) {
-    return (12 * nnz) / 128 + 2 * nrows + 2;
+// Row kinds: SMALL rows share windowed tiles; a MEDIUM row (not small, but
+// products + 4*entries + 4 <= PMAX and every B row it reads <= SP_LEN_MAX
+// long) is a tile of its own; BIG rows go to the side path.
+enum : int8_t { RK_SMALL = 0, RK_MEDIUM = 1, RK_BIG = 2 };
+
+// Row weight: tiles are runs of small rows within one TW-window of the
+// exclusive prefix of weights, so a tile has < PMAX products, < PMAX/4
+// entries and < PMAX/4 rows.
+__host__ __device__ __forceinline__ int64_t tile_weight(int64_t p, int64_t ne) { return p + 4 * ne + 4; }
+__host__ __device__ __forceinline__ bool tile_small(int64_t p, int64_t ne) {
+    return p <= tile::SMALL_P && ne <= tile::SMALL_E;
 }
 
-enum : int8_t { RK_SMALL = 0, RK_BIG = 1 };
-
-// ------------------------------------------------------------- PTX helpers
-__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ bool mbar_try(uint64_t* b, unsigned parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(ok)
-        : "r"(su32(b)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-// Non-blocking probe of a phase (try_wait may suspend the thread for a while).
-__device__ __forceinline__ bool mbar_test(uint64_t* b, unsigned parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(ok)
-        : "r"(su32(b)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-// Waits for the phase of `parity` to complete, backing off with nanosleep so
-// that waiting warps do not take issue slots from working ones. A wait longer
-// than ~20 s of SM clock traps (a scheduling bug must fail the launch, not
-// hang the device).
-__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
-    if (mbar_try(b, parity)) return;
-    const long long t0 = clock64();
-    unsigned ns = 32;
-    while (!mbar_try(b, parity)) {
-        __nanosleep(ns);
-        ns = min(ns * 2, 256u);
-        if (clock64() - t0 > 40000000000ll) __trap();
-    }
-}
-// 16-byte global -> shared copy (LDGSTS), completion tracked by wait_group.
-__device__ __forceinline__ void cp16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-// Bulk (TMA) global -> shared copy completing on an mbarrier's transaction count.
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
-        "l"(src), "r"(bytes), "r"(su32(bar))
-        : "memory");
-}
-
-// Decoupled look-back status word: bits 62-63 flag (0 none, 1 aggregate,
-// 2 inclusive prefix), bits 0-61 value.
-constexpr uint64_t ST_AGG = 1ull << 62, ST_INC = 2ull << 62, ST_VAL = (1ull << 62) - 1;
-
-__device__ __forceinline__ uint64_t ld_status(const uint64_t* p) {
-    uint64_t v;
-    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_status(uint64_t* p, uint64_t v) {
-    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-#ifdef SPG_MERGE_PROF
-// Dev instrumentation (-DSPG_MERGE_PROF): clock64 totals per role phase, lane 0.
-__device__ unsigned long long g_merge_prof[24];
-#define MP_DECL long long mp_last_ = clock64(), mp_acc_[24] = {0};
-#define MP(i)                                   \
-    do {                                        \
-        const long long t_ = clock64();         \
-        mp_acc_[i] += t_ - mp_last_;            \
-        mp_last_ = t_;                          \
-    } while (0)
-#define MP_CNT(i) mp_acc_[i] += 1
-#define MP_FLUSH                                                                                  \
-    if ((threadIdx.x & 31) == 0)                                                                  \
-        for (int i_ = 0; i_ < 24; ++i_)                                                           \
-            if (mp_acc_[i_]) atomicAdd(&g_merge_prof[i_], static_cast<unsigned long long>(mp_acc_[i_]));
-#else
-#define MP_DECL
-#define MP(i)
-#define MP_CNT(i)
-#define MP_FLUSH
-#endif
-
-// ------------------------------------------------------------- row plan
-// Half a warp per row of A (two rows in flight per warp: the row is a chain of
-// dependent loads arp -> acol -> brp). Per row: products, kind and the tile
-// weight of a SMALL row; per entry the packed B block and the B row length.
-// A row is SMALL when its staged slots (sum of roundup4(len)) fit a worker
-// row and its weight sum(max(roundup4(len), EMIN)) + EMIN fits RW.
-__global__ void k_row_plan(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
+// Per row (warp per row, lanes over entries): products(i) = Σ nnz(B_k), the
+// row kind, the packed entry spans of tile rows (so the tile kernel reads its
+// entries with no dependent B.rowptr load and no row pass), the row weight,
+// and the BIG-row lists: 0 = CTA rows (<= CTA_P products, <= CTA_E entries),
+// 1 = heavy.
+__global__ void k_row_prep(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
                            const int64_t* __restrict__ brp, int64_t m, int64_t* __restrict__ prod,
                            int64_t* __restrict__ wt, int8_t* __restrict__ kind, uint64_t* __restrict__ espan,
                            int32_t* __restrict__ big_rows, int32_t* __restrict__ nbig) {
+    // half-warp per row (two rows in flight per warp: the row is a chain of
+    // dependent loads arp -> acol -> brp); loops are warp-uniform
     const int lane = threadIdx.x & 31, sub = lane & 15, half = lane >> 4;
     const int64_t gw = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
     const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -219,47 +120,93 @@ __global__ void k_row_plan(const int64_t* __restrict__ arp, const int32_t* __res
         }
         const int64_t ne = e1 - e0;
         const int64_t ne_max = max(ne, static_cast<int64_t>(__shfl_xor_sync(FULL, ne, 16)));
-        int64_t p = 0, slots = 0, w = 0;
+        int64_t p = 0, maxlen = 0, bsr[2] = {0, 0}, lenr[2] = {0, 0};  // rows of <= 32 entries keep their spans
         for (int64_t t = 0; t < ne_max; t += 16) {
-            int64_t len = 0, l4 = 0, we = 0;
+            int64_t bs = 0, len = 0;
             if (t + sub < ne) {
                 const int32_t k = __ldg(acol + e0 + t + sub);
-                const int64_t bs = __ldg(brp + k);
+                bs = __ldg(brp + k);
                 len = __ldg(brp + k + 1) - bs;
-                l4 = (len + 3) & ~int64_t(3);
-                we = max(l4, int64_t(mg::EMIN));
-                espan[e0 + t + sub] = (block_of(bs, k) << 32) | static_cast<uint64_t>(min(len, int64_t(0xffffffff)));
             }
+            if (t == 0) {  // (the other half's row may take more iterations)
+                bsr[0] = bs;
+                lenr[0] = len;
+            } else if (t == 16) {
+                bsr[1] = bs;
+                lenr[1] = len;
+            }
+            int64_t sum = len;
 #pragma unroll
-            for (int o = 8; o > 0; o >>= 1) {
-                len += __shfl_xor_sync(FULL, len, o);
-                l4 += __shfl_xor_sync(FULL, l4, o);
-                we += __shfl_xor_sync(FULL, we, o);
-            }
-            p += len;
-            slots += l4;
-            w += we;
+            for (int o = 8; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+            p += sum;
+            maxlen = max(maxlen, len);
         }
-        w += mg::EMIN;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) maxlen = max(maxlen, static_cast<int64_t>(__shfl_xor_sync(FULL, maxlen, o)));
+        int8_t rk = RK_BIG;
+        if (tile_small(p, ne)) rk = RK_SMALL;
+        else if (tile_weight(p, ne) <= tile::PMAX && maxlen <= tile::SP_LEN_MAX) rk = RK_MEDIUM;
+        const uint64_t pr = static_cast<uint64_t>(p);
+        const bool spans = ok && rk != RK_BIG;
+        {  // rows of <= 32 entries: in-row product offsets from registers
+            int64_t carry = 0;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                int64_t inc = lenr[c];
+#pragma unroll
+                for (int o = 1; o < 16; o <<= 1) {
+                    const int64_t y = __shfl_up_sync(FULL, inc, o, 16);
+                    if (sub >= o) inc += y;
+                }
+                if (spans && ne <= 32 && 16 * c + sub < ne)
+                    espan[e0 + 16 * c + sub] = (static_cast<uint64_t>(bsr[c]) & tile::SP_BS_MASK) |
+                                               (static_cast<uint64_t>(lenr[c]) << tile::SP_LEN) |
+                                               (static_cast<uint64_t>(carry + inc - lenr[c]) << tile::SP_IN) |
+                                               (pr << tile::SP_PR);
+                carry += __shfl_sync(FULL, inc, 15, 16);
+            }
+        }
+        const bool slow = spans && ne > 32;
+        if (__any_sync(FULL, slow)) {  // longer rows: a second pass
+            int64_t carry = 0;
+            for (int64_t t = 0; t < ne_max; t += 16) {
+                int64_t bs = 0, len = 0;
+                if (slow && t + sub < ne) {
+                    const int32_t k = __ldg(acol + e0 + t + sub);
+                    bs = __ldg(brp + k);
+                    len = __ldg(brp + k + 1) - bs;
+                }
+                int64_t inc = len;
+#pragma unroll
+                for (int o = 1; o < 16; o <<= 1) {
+                    const int64_t y = __shfl_up_sync(FULL, inc, o, 16);
+                    if (sub >= o) inc += y;
+                }
+                if (slow && t + sub < ne)
+                    espan[e0 + t + sub] = (static_cast<uint64_t>(bs) & tile::SP_BS_MASK) |
+                                          (static_cast<uint64_t>(len) << tile::SP_LEN) |
+                                          (static_cast<uint64_t>(carry + inc - len) << tile::SP_IN) |
+                                          (pr << tile::SP_PR);
+                carry += __shfl_sync(FULL, inc, 15, 16);
+            }
+        }
         if (ok && sub == 0) {
-            const bool small = slots <= mg::RS && w <= mg::RW;
             prod[i] = p;
-            kind[i] = small ? RK_SMALL : RK_BIG;
-            wt[i] = small ? w : 0;
-            if (!small) big_rows[atomicAdd(nbig, 1)] = static_cast<int32_t>(i);
+            kind[i] = rk;
+            wt[i] = rk == RK_SMALL ? tile_weight(p, ne) : 0;
+            if (rk == RK_BIG) big_rows[atomicAdd(nbig, 1)] = static_cast<int32_t>(i);
         }
     }
 }
 
-// Tile starts: row i starts a tile if it is BIG, follows a BIG row, or its
-// weight prefix enters a new TW-window (so a tile of SMALL rows has weight
-// < TW + RW = TS).
+// Tile starts: row i starts a tile if it is not SMALL, follows a row that is
+// not SMALL, or its weight prefix enters a new TW-window.
 __global__ void k_tile_flags(const int64_t* __restrict__ wpre, const int8_t* __restrict__ kind, int64_t m,
                              int64_t* __restrict__ flag) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
         int f = 1;
         if (i > 0 && kind[i] == RK_SMALL)
-            f = kind[i - 1] != RK_SMALL || (wpre[i] / mg::TW != wpre[i - 1] / mg::TW);
+            f = kind[i - 1] != RK_SMALL || (wpre[i] / tile::TW != wpre[i - 1] / tile::TW);
         flag[i] = f;
     }
 }
@@ -279,630 +226,6 @@ __global__ void k_tile_scatter(const int64_t* __restrict__ flag, const int64_t* 
             te[fpos[i]] = arp[i];
         }
     }
-}
-
-// B -> packed row blocks (block_of): a warp per row, columns then values, each
-// padded to a multiple of 4 (pad columns -1, pad values 0).
-__global__ void k_pack_rows(const int64_t* __restrict__ brp, const int32_t* __restrict__ bcol,
-                            const double* __restrict__ bval, int64_t n, unsigned char* __restrict__ bp) {
-    const int lane = threadIdx.x & 31;
-    const int64_t gw = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
-    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t k = gw; k < n; k += nw) {
-        const int64_t b0 = brp[k], len = brp[k + 1] - b0, l4 = (len + 3) & ~int64_t(3);
-        int32_t* dc = reinterpret_cast<int32_t*>(bp + block_of(b0, k) * 128);
-        double* dv = reinterpret_cast<double*>(dc + l4);
-        for (int64_t t = lane; t < l4; t += 32) {
-            const bool in = t < len;
-            dc[t] = in ? __ldg(bcol + b0 + t) : -1;
-            dv[t] = in ? __ldg(bval + b0 + t) : 0.0;
-        }
-    }
-}
-
-// ------------------------------------------------------------- k_merge
-namespace mg {
-enum : int { F_BIG = 1, F_END = 2 };
-struct Hdr {
-    int64_t k, r0, e0;
-    int R, E, flags;
-    int claim, slots;       // row claims, slot allocation
-    int rows_done, nnz;     // finished rows and their nnz (the tile's aggregate)
-};
-struct __align__(16) Stage {
-    double val[TS];            // staged products' values, then the rows' C values
-    int32_t col[TS];           // staged products' columns, then the rows' C columns
-    uint64_t espan[TE + 2];    // tile entries' B blocks (element i - (e0 & ~1))
-    double aval[TE + 2];       // tile entries' A values
-    int64_t arp[TR + 4];       // tile row pointers (element i - (r0 & ~1))
-    uint16_t q[TS / 4];        // tile entry of each staged slot quad
-    uint16_t rs0[TR];          // first slot of each row
-    uint16_t perm[TS];         // per row position: the slot holding its C entry (bit 15: hole)
-    uint16_t rnnz[TR];         // nnz of each row's C
-    uint16_t rsrc[TR];         // staged C entries of each row (bit 15: holes among them)
-    Hdr hdr;
-};
-struct __align__(16) Worker {
-    uint32_t cnt[CW];          // bucket counters (gather: entry slot offsets)
-    uint16_t rk[RS];           // per slot: rank in its bucket
-    uint16_t pa[RS];           // per bucket position: the slot placed there
-};
-struct __align__(16) Smem {
-    Stage st[NST];
-    Worker wk[NWORK];
-    uint64_t ready[NST];       // setup -> workers/epilogue: the stage holds tile t
-    uint64_t done[NST];        // workers -> epilogue: every worker is past tile t
-    uint64_t freed[NST];       // epilogue -> setup: the stage is free
-};
-static_assert(sizeof(Smem) <= 227 * 1024, "k_merge shared memory exceeds 227 KB");
-}  // namespace mg
-
-// Copies elements [i0, i1) of an 8-byte array g into s so that element i lands
-// at s[i - (i0 & ~1)]: the 16-byte-aligned middle by one bulk copy, an odd
-// tail element by the calling lane. Returns the bulk bytes (for expect_tx).
-__device__ __forceinline__ unsigned stage_slice8(void* s, const void* g, int64_t i0, int64_t i1, uint64_t* bar,
-                                                 int lane, bool issue) {
-    const int64_t ib = i0 & ~int64_t(1), ie = i1 & ~int64_t(1);
-    const unsigned bytes = ie > ib ? static_cast<unsigned>(8 * (ie - ib)) : 0u;
-    if (issue) {
-        if (bytes) bulk_g2s(s, static_cast<const uint64_t*>(g) + ib, bytes, bar);
-    } else if (lane == 0 && (i1 & 1) && i1 - 1 >= i0) {
-        static_cast<uint64_t*>(s)[i1 - 1 - ib] = __ldg(static_cast<const unsigned long long*>(g) + (i1 - 1));
-    }
-    return bytes;
-}
-
-// Setup warp: tickets -> stages. Publishes END into NEPI consecutive stages so
-// that every epilogue warp meets one.
-__device__ void merge_setup(mg::Smem& S, const int64_t* __restrict__ arp, const double* __restrict__ aval,
-                            const uint64_t* __restrict__ espan, const int64_t* __restrict__ tr,
-                            const int64_t* __restrict__ te, int64_t ntiles, unsigned long long* ticket,
-                            const int64_t* __restrict__ side_nnz, uint64_t* __restrict__ status) {
-    using namespace mg;
-    const int lane = threadIdx.x & 31;
-    int nend = 0;
-    MP_DECL
-    for (int t = 0;; ++t) {
-        const int s = t % NST;
-        MP(6);
-        mbar_wait(&S.freed[s], ((t / NST) & 1) ^ 1);
-        MP(5);
-        MP_CNT(7);
-        Stage& G = S.st[s];
-        // the ticket is taken only once the stage is free: a tile ticketed is a
-        // tile staged, so look-backs never wait on a ticket parked in a setup warp
-        int64_t tk = 0;
-        if (lane == 0) tk = static_cast<int64_t>(atomicAdd(ticket, 1ull));
-        tk = __shfl_sync(FULL, tk, 0);
-        if (tk >= ntiles) {
-            if (lane == 0) {
-                G.hdr.flags = F_END;
-                mbar_arrive(&S.ready[s]);
-            }
-            if (++nend == NEPI) break;
-            continue;
-        }
-        const int64_t k = tk;
-        int64_t v = 0;
-        if (lane < 4) v = __ldg((lane & 1 ? te : tr) + k + (lane >> 1));
-        const int64_t trk = __shfl_sync(FULL, v, 0), e0 = __shfl_sync(FULL, v, 1);
-        const int64_t trk1 = __shfl_sync(FULL, v, 2), e1 = __shfl_sync(FULL, v, 3);
-        const int64_t mask = (int64_t(1) << 62) - 1;
-        const int64_t r0 = trk & mask, r1 = trk1 & mask;
-        const bool big = (trk >> 62) != 0;
-        if (lane == 0) {
-            G.hdr.k = k;
-            G.hdr.r0 = r0;
-            G.hdr.e0 = e0;
-            G.hdr.R = static_cast<int>(r1 - r0);
-            G.hdr.E = static_cast<int>(e1 - e0);
-            G.hdr.flags = big ? F_BIG : 0;
-            G.hdr.claim = 0;
-            G.hdr.slots = 0;
-            G.hdr.rows_done = 0;
-            G.hdr.nnz = 0;
-        }
-        if (big) {
-            // the side path sized the row already: publish the aggregate now
-            if (lane == 0) st_status(status + k, (k == 0 ? ST_INC : ST_AGG) | static_cast<uint64_t>(side_nnz[r0]));
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&S.ready[s]);
-        } else {
-            // odd tails by plain loads, then arm the barrier and issue the bulk copies
-            unsigned bytes = stage_slice8(G.espan, espan, e0, e1, &S.ready[s], lane, false);
-            bytes += stage_slice8(G.aval, aval, e0, e1, &S.ready[s], lane == 1 ? 0 : 1, false);
-            bytes += stage_slice8(G.arp, arp, r0, r1 + 1, &S.ready[s], lane == 2 ? 0 : 1, false);
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive_tx(&S.ready[s], bytes);
-                stage_slice8(G.espan, espan, e0, e1, &S.ready[s], 0, true);
-                stage_slice8(G.aval, aval, e0, e1, &S.ready[s], 0, true);
-                stage_slice8(G.arp, arp, r0, r1 + 1, &S.ready[s], 0, true);
-            }
-        }
-    }
-    MP_FLUSH
-}
-
-// Per-worker state of a claimed row.
-struct RowJob {
-    int s, j, t;
-    int S0, ns;  // first slot, slots
-};
-
-// Issues the cp.async gathers of row j of stage s (one commit group) and
-// allocates its slots. The B block of an entry is contiguous: chunk c of the
-// block goes to the column region for c < len4/4, else to the value region.
-__device__ __forceinline__ void merge_gather(mg::Smem& S, RowJob& R, uint32_t* scratch,
-                                             const unsigned char* __restrict__ bp) {
-    using namespace mg;
-    const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
-    Stage& G = S.st[R.s];
-    const int64_t r0 = G.hdr.r0, e0 = G.hdr.e0;
-    const int ro = static_cast<int>(r0 & 1), eo = static_cast<int>(e0 & 1);
-    const int eb = static_cast<int>(G.arp[R.j + ro] - e0), ee = static_cast<int>(G.arp[R.j + 1 + ro] - e0);
-    const int ne = ee - eb;  // <= 79 for a SMALL row
-    int tot = 0;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        if (32 * c >= ne) break;
-        const int q = 32 * c + lane;
-        int l4 = 0;
-        if (q < ne) l4 = (static_cast<int>(static_cast<uint32_t>(G.espan[eb + q + eo])) + 3) & ~3;
-        const int inc = warp_inclusive_scan(l4);
-        if (q < ne) scratch[q] = static_cast<uint32_t>(tot + inc - l4);
-        tot += __shfl_sync(FULL, inc, 31);
-    }
-    int S0 = 0;
-    if (lane == 0) {
-        S0 = atomicAdd(&G.hdr.slots, tot);
-        G.rs0[R.j] = static_cast<uint16_t>(S0);
-    }
-    S0 = __shfl_sync(FULL, S0, 0);
-    R.S0 = S0;
-    R.ns = tot;
-    __syncwarp();
-    // slot quad -> tile entry
-    for (int q = lane; q < ne; q += 32) {
-        const int l4 = (static_cast<int>(static_cast<uint32_t>(G.espan[eb + q + eo])) + 3) & ~3;
-        const int qb = (S0 + static_cast<int>(scratch[q])) >> 2;
-        for (int u = 0; u < (l4 >> 2); ++u) G.q[qb + u] = static_cast<uint16_t>(eb + q);
-    }
-    // gathers: half a warp per entry
-    for (int q0 = 0; q0 < ne; q0 += 2) {
-        const int q = q0 + half;
-        if (q < ne) {
-            const uint64_t sp = G.espan[eb + q + eo];
-            const int l4 = (static_cast<int>(static_cast<uint32_t>(sp)) + 3) & ~3;
-            const int nc4 = l4 >> 2, nc = 3 * nc4;
-            const int sl = S0 + static_cast<int>(scratch[q]);
-            const unsigned char* src = bp + (sp >> 32) * 128;
-            unsigned char* dcol = reinterpret_cast<unsigned char*>(G.col + sl);
-            unsigned char* dval = reinterpret_cast<unsigned char*>(G.val + sl) - 16 * nc4;
-            for (int c = hl; c < nc; c += 16) cp16((c < nc4 ? dcol : dval) + 16 * c, src + 16 * c);
-        }
-    }
-    cp_commit();
-}
-
-#ifdef SPG_MERGE_PROF
-#define SP(i)                                  \
-    do {                                       \
-        const long long t_ = clock64();        \
-        sp[i] += t_ - sp_last;                 \
-        sp_last = t_;                          \
-    } while (0)
-#else
-#define SP(i)
-#endif
-// Sorts a gathered row without moving its entries: every slot's value
-// becomes 0 + a*b in place, and perm[q] (q in [0, p), p the row's products)
-// names the slot of the q-th C entry in column order. Equal columns are
-// summed into the first of their run in slot order (= ascending k); the
-// others are marked as holes (bit 15) that the copy-out skips. Returns
-// p | holes << 16.
-__device__ __noinline__ uint32_t merge_sort_row(mg::Smem& S, const RowJob& R, mg::Worker& W
-#ifdef SPG_MERGE_PROF
-                                                , long long* sp
-#endif
-) {
-    using namespace mg;
-    const int lane = threadIdx.x & 31;
-#ifdef SPG_MERGE_PROF
-    long long sp_last = clock64();
-#endif
-    Stage& G = S.st[R.s];
-    const int S0 = R.S0, ns = R.ns;
-    const int eo = static_cast<int>(G.hdr.e0 & 1);
-    const int32_t* col = G.col + S0;
-    double* val = G.val + S0;
-    uint16_t* pb = G.perm + S0;
-    const int nw = (ns + 31) >> 5;
-    // column range of the row (padding slots hold -1)
-    uint32_t cmin = 0xffffffffu;
-    int cmax = -1;
-    for (int i = 0; i < nw; ++i) {
-        const int sl = 32 * i + lane;
-        const int c = sl < ns ? col[sl] : -1;
-        cmin = min(cmin, static_cast<uint32_t>(c));
-        cmax = max(cmax, c);
-    }
-    cmin = __reduce_min_sync(FULL, cmin);
-    cmax = static_cast<int>(__reduce_max_sync(FULL, static_cast<unsigned>(max(cmax, 0))));
-    SP(0);
-    if (cmin == 0xffffffffu) return 0;  // no products (empty B rows only)
-    // buckets: nb in [256, BPS * RS], monotone in the column over the row's range
-    const int nb = max(256, (BPS * ns + 255) & ~255);
-    const int K = nb >> 5;  // bucket words per lane
-    const int sh = __clz(max(static_cast<uint32_t>(cmax) - cmin, 1u));
-    uint32_t* cnt = W.cnt;
-    for (int u = 0; u < (K >> 2); ++u) reinterpret_cast<uint4*>(cnt + lane * K)[u] = make_uint4(0, 0, 0, 0);
-    __syncwarp();
-    // values (0 + a*b, in place), then each product's rank in its bucket:
-    // every product writes its slot into the bucket's claim tag, the one that
-    // reads its own slot back has rank 0, the others take 1 + an atomic count
-    // (rank order within a bucket is arbitrary; the ordering below sorts a
-    // bucket of several by (column, slot))
-    uint16_t* tag = reinterpret_cast<uint16_t*>(cnt) + 1;  // high half of each bucket word
-#pragma unroll 4
-    for (int i = 0; i < nw; ++i) {
-        const int sl = 32 * i + lane;
-        if (sl < ns) {
-            const int c = col[sl];
-            const double bv = val[sl];
-            const double av = G.aval[G.q[(S0 + sl) >> 2] + eo];
-            val[sl] = dadd(0.0, dmul(av, bv));
-            if (c >= 0) {
-                const uint32_t b = __umulhi((static_cast<uint32_t>(c) - cmin) << sh, static_cast<uint32_t>(nb));
-                tag[2 * b] = static_cast<uint16_t>(sl + 1);
-            }
-        }
-    }
-    __syncwarp();
-#pragma unroll 4
-    for (int i = 0; i < nw; ++i) {
-        const int sl = 32 * i + lane;
-        const int c = sl < ns ? col[sl] : -1;
-        if (c >= 0) {
-            const uint32_t b = __umulhi((static_cast<uint32_t>(c) - cmin) << sh, static_cast<uint32_t>(nb));
-            uint32_t rank = 0;
-            if (tag[2 * b] != sl + 1) rank = 1u + (atomicAdd(&cnt[b], 1u) & 0xffffu);
-            W.rk[sl] = static_cast<uint16_t>(rank);
-        }
-    }
-    __syncwarp();
-    SP(1);
-    // exclusive scan of the bucket sizes (claimed + extra): word b becomes E[b]
-    uint32_t* wp = cnt + lane * K;
-    constexpr int KMAX = BPS * RS / 32;
-    uint32_t wv[KMAX];
-    int sum = 0;
-#pragma unroll
-    for (int u = 0; u < KMAX; ++u) {
-        wv[u] = 0;
-        if (u < K) {
-            const uint32_t x = wp[u];
-            wv[u] = (x >> 16 ? 1u : 0u) + (x & 0xffffu);
-        }
-        sum += static_cast<int>(wv[u]);
-    }
-    const int inc = warp_inclusive_scan(sum);
-    const int total = __shfl_sync(FULL, inc, 31);
-    {
-        uint32_t e = static_cast<uint32_t>(inc - sum);
-#pragma unroll
-        for (int u = 0; u < KMAX; ++u) {
-            if (u < K) wp[u] = e;
-            e += wv[u];
-        }
-    }
-    if (lane == 31) cnt[nb] = static_cast<uint32_t>(total);
-    __syncwarp();
-    SP(2);
-    // place: a product alone in its bucket is final; buckets of several are
-    // listed by position (pa) and ordered below
-    bool multi = false;
-#pragma unroll 2
-    for (int i = 0; i < nw; ++i) {
-        const int sl = 32 * i + lane;
-        const int c = sl < ns ? col[sl] : -1;
-        if (c >= 0) {
-            const uint32_t b = __umulhi((static_cast<uint32_t>(c) - cmin) << sh, static_cast<uint32_t>(nb));
-            const uint32_t st = cnt[b], n = cnt[b + 1] - st;
-            const int pos = static_cast<int>(st) + W.rk[sl];
-            if (n == 1) {
-                pb[pos] = static_cast<uint16_t>(sl);
-            } else {
-                W.pa[pos] = static_cast<uint16_t>(sl);
-                multi = true;
-            }
-        }
-    }
-    SP(3);
-    if (!__any_sync(FULL, multi)) return static_cast<uint32_t>(total);
-    __syncwarp();
-    // buckets of several: each product's place in (column, slot) order from
-    // its mates; a product equal in column to a mate of smaller slot becomes
-    // a hole, and the first of a run sums the run in slot order (= ascending k)
-    int holes = 0;
-    for (int i = 0; i < nw; ++i) {
-        const int sl = 32 * i + lane;
-        const int c = sl < ns ? col[sl] : -1;
-        if (c < 0) continue;
-        const uint32_t b = __umulhi((static_cast<uint32_t>(c) - cmin) << sh, static_cast<uint32_t>(nb));
-        const int st = static_cast<int>(cnt[b]), n = static_cast<int>(cnt[b + 1]) - st;
-        if (n < 2) continue;
-        int lo = 0, eqb = 0, eqa = 0;
-        for (int u = 0; u < n; ++u) {
-            const int s2 = W.pa[st + u];
-            const int mc = col[s2];
-            lo += mc < c ? 1 : 0;
-            eqb += (mc == c && s2 < sl) ? 1 : 0;
-            eqa += (mc == c && s2 > sl) ? 1 : 0;
-        }
-        pb[st + lo + eqb] = static_cast<uint16_t>(sl | (eqb ? 0x8000 : 0));
-        if (eqb) {
-            ++holes;
-        } else if (eqa) {
-            // followers in slot order: repeatedly the smallest equal slot above the last
-            double acc = val[sl];
-            int last = sl;
-            for (int f = 0; f < eqa; ++f) {
-                int nxt = 0x7fffffff;
-                for (int u = 0; u < n; ++u) {
-                    const int s2 = W.pa[st + u];
-                    if (s2 > last && s2 < nxt && col[s2] == c) nxt = s2;
-                }
-                acc = dadd(acc, val[nxt]);
-                last = nxt;
-            }
-            val[sl] = acc;
-        }
-    }
-    holes = __reduce_add_sync(FULL, holes);
-    SP(4);
-    return static_cast<uint32_t>(total) | (static_cast<uint32_t>(holes) << 16);
-}
-
-// Row worker: claim -> gather (one row ahead) -> sort. A worker arrives on a
-// tile's `done` barrier once it has moved past the tile and finished its own
-// rows of it (the pending row of the tile, if any, is finished first). The
-// pending row is also finished before the worker blocks on a stage that is
-// not staged yet.
-__device__ void merge_worker(mg::Smem& S, int w, const unsigned char* __restrict__ bp, uint64_t* __restrict__ status) {
-    using namespace mg;
-    const int lane = threadIdx.x & 31;
-    Worker& W = S.wk[w];
-    int cur = 0;
-    RowJob P{-1, 0, 0, 0, 0};
-    bool owe = false;
-    MP_DECL
-#ifdef SPG_MERGE_PROF
-    long long sp_acc[5] = {0, 0, 0, 0, 0};
-#endif
-    auto finish = [&](bool one_in_flight) {
-        MP(1);
-        if (one_in_flight) cp_wait<1>();
-        else cp_wait<0>();
-        __syncwarp();
-        MP(2);
-#ifdef SPG_MERGE_PROF
-        const uint32_t res = merge_sort_row(S, P, W, sp_acc);
-#else
-        const uint32_t res = merge_sort_row(S, P, W);
-#endif
-        const int nnz = static_cast<int>((res & 0xffffu) - (res >> 16));
-        MP(3);
-        MP_CNT(4);
-        if (lane == 0) {
-            // the worker finishing a tile's last row publishes the tile's
-            // aggregate at once (not behind the epilogue's look-backs)
-            Hdr& H = S.st[P.s].hdr;
-            S.st[P.s].rnnz[P.j] = static_cast<uint16_t>(nnz);
-            S.st[P.s].rsrc[P.j] = static_cast<uint16_t>((res & 0xffffu) | (res >> 16 ? 0x8000u : 0u));
-            atomicAdd(&H.nnz, nnz);
-            __threadfence_block();
-            if (atomicAdd(&H.rows_done, 1) == H.R - 1) {
-                const int agg = atomicAdd(&H.nnz, 0);
-                st_status(status + H.k, (H.k == 0 ? ST_INC : ST_AGG) | static_cast<uint64_t>(agg));
-            }
-        }
-        if (owe) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&S.done[P.s]);
-        }
-        P.s = -1;
-        owe = false;
-        MP(14);
-    };
-    while (true) {
-        RowJob N{-1, 0, 0, 0, 0};
-        while (true) {
-            const int s = cur % NST;
-            // never block on a stage while a gathered row is pending: the
-            // pending row may be the last of a tile whose aggregate the
-            // look-backs (and so the refill of this stage) wait for
-            if (P.s >= 0 && !mbar_test(&S.ready[s], (cur / NST) & 1)) finish(false);
-            MP(1);
-            mbar_wait(&S.ready[s], (cur / NST) & 1);
-            MP(0);
-            Hdr& H = S.st[s].hdr;
-            const int flags = *reinterpret_cast<volatile int*>(&H.flags);
-            if (flags & F_END) break;
-            if (!(flags & F_BIG)) {
-                int j = 0;
-                if (lane == 0) j = atomicAdd(&H.claim, 1);
-                j = __shfl_sync(FULL, j, 0);
-                if (j < H.R) {
-                    N.s = s;
-                    N.j = j;
-                    N.t = cur;
-                    break;
-                }
-            }
-            if (P.s >= 0 && P.t == cur) owe = true;
-            else if (lane == 0) mbar_arrive(&S.done[s]);
-            ++cur;
-        }
-        MP(1);
-        if (N.s >= 0) merge_gather(S, N, W.cnt, bp);
-        MP(13);
-        if (P.s >= 0) finish(N.s >= 0);
-        if (N.s < 0) break;
-        P = N;
-    }
-#ifdef SPG_MERGE_PROF
-    for (int i = 0; i < 5; ++i) mp_acc_[16 + i] += sp_acc[i];
-#endif
-    MP_FLUSH
-}
-
-// Exclusive prefix of tile k (one warp, 128 predecessors per round trip).
-#ifdef SPG_MERGE_PROF
-__device__ unsigned long long g_lb_prof[4];
-#endif
-__device__ __forceinline__ int64_t merge_look_back(const uint64_t* status, int64_t k) {
-    const int lane = threadIdx.x & 31;
-    int64_t excl = 0;
-    for (int64_t j0 = k - 1;; j0 -= 128) {
-#ifdef SPG_MERGE_PROF
-        if (lane == 0) atomicAdd(&g_lb_prof[0], 1ull);
-#endif
-        uint64_t sv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int64_t idx = j0 - (32 * u + lane);
-            sv[u] = idx >= 0 ? ld_status(status + idx) : ST_INC;
-        }
-        int first = 128;
-        const long long t0 = clock64();
-        while (true) {
-            first = 128;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const unsigned mk = __ballot_sync(FULL, (sv[u] >> 62) == 2);
-                if (mk && first == 128) first = 32 * u + __ffs(mk) - 1;
-            }
-            bool wait = false;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) wait |= (32 * u + lane <= first) && (sv[u] >> 62) == 0;
-            if (!__any_sync(FULL, wait)) break;
-            if (clock64() - t0 > 40000000000ll) __trap();
-#ifdef SPG_MERGE_PROF
-            if (lane == 0) atomicAdd(&g_lb_prof[1], 1ull);
-#endif
-            __nanosleep(64);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int64_t idx = j0 - (32 * u + lane);
-                if ((32 * u + lane <= first) && (sv[u] >> 62) == 0) sv[u] = ld_status(status + idx);
-            }
-        }
-        int64_t part = 0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (32 * u + lane <= first) part += static_cast<int64_t>(sv[u] & ST_VAL);
-        excl += warp_reduce_sum(part);
-        if (first < 128) break;
-    }
-    return excl;
-}
-
-// Epilogue warp e: tiles t = e, e + NEPI, ... of this CTA.
-__device__ void merge_epilogue(mg::Smem& S, int e, uint64_t* __restrict__ status,
-                               const int64_t* __restrict__ side_nnz, int64_t* __restrict__ crp,
-                               int32_t* __restrict__ ccol, double* __restrict__ cval) {
-    using namespace mg;
-    const int lane = threadIdx.x & 31;
-    MP_DECL
-    for (int t = e;; t += NEPI) {
-        const int s = t % NST;
-        const unsigned par = (t / NST) & 1;
-        MP(10);
-        mbar_wait(&S.ready[s], par);
-        Stage& G = S.st[s];
-        if (*reinterpret_cast<volatile int*>(&G.hdr.flags) & F_END) break;
-        mbar_wait(&S.done[s], par);
-        MP(8);
-        MP_CNT(11);
-        const int64_t k = G.hdr.k, r0 = G.hdr.r0;
-        const int R = G.hdr.R;
-        const bool big = (G.hdr.flags & F_BIG) != 0;
-        // the tile's aggregate is already published (setup for a BIG tile,
-        // the worker of the last row otherwise)
-        const int64_t agg = big ? side_nnz[r0] : static_cast<int64_t>(G.hdr.nnz);
-        MP(10);
-        const int64_t excl = k == 0 ? 0 : merge_look_back(status, k);
-        MP(9);
-        if (lane == 0 && k > 0) st_status(status + k, ST_INC | static_cast<uint64_t>(excl + agg));
-        if (big) {
-            if (lane == 0) crp[r0 + 1] = excl + agg;
-        } else {
-            int64_t carry = excl;
-            for (int c0 = 0; c0 < R; c0 += 32) {
-                const int j = c0 + lane;
-                const int nj = j < R ? G.rnnz[j] : 0;
-                const int inc = warp_inclusive_scan(nj);
-                if (j < R) crp[r0 + j + 1] = carry + inc;
-                const int nr = min(32, R - c0);
-                for (int jj = 0; jj < nr; ++jj) {
-                    const int n = __shfl_sync(FULL, nj, jj);
-                    const int64_t o = carry + __shfl_sync(FULL, inc, jj) - n;
-                    const int s0 = G.rs0[c0 + jj], src = G.rsrc[c0 + jj], p = src & 0x7fff;
-                    const uint16_t* pm = G.perm + s0;
-                    if (!(src & 0x8000)) {
-                        for (int qq = lane; qq < p; qq += 32) {
-                            const int sl = s0 + pm[qq];
-                            ccol[o + qq] = G.col[sl];
-                            cval[o + qq] = G.val[sl];
-                        }
-                    } else {  // duplicates left holes: compact while copying
-                        int64_t d = o;
-                        for (int q0 = 0; q0 < p; q0 += 32) {
-                            const int qq = q0 + lane;
-                            const int e = qq < p ? pm[qq] : 0x8000;
-                            const bool keep = !(e & 0x8000);
-                            const unsigned km = __ballot_sync(FULL, keep);
-                            if (keep) {
-                                const int64_t at = d + __popc(km & ((1u << lane) - 1u));
-                                ccol[at] = G.col[s0 + e];
-                                cval[at] = G.val[s0 + e];
-                            }
-                            d += __popc(km);
-                        }
-                    }
-                }
-                carry += __shfl_sync(FULL, inc, 31);
-            }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&S.freed[s]);
-    }
-    MP_FLUSH
-}
-
-__global__ void __launch_bounds__(mg::NT, 1)
-    k_merge(const int64_t* __restrict__ arp, const double* __restrict__ aval, const uint64_t* __restrict__ espan,
-            const unsigned char* __restrict__ bp, const int64_t* __restrict__ tr, const int64_t* __restrict__ te,
-            int64_t ntiles, unsigned long long* __restrict__ ticket, const int64_t* __restrict__ side_nnz,
-            uint64_t* __restrict__ status, int64_t* __restrict__ crp, int32_t* __restrict__ ccol,
-            double* __restrict__ cval) {
-    using namespace mg;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    Smem& S = *reinterpret_cast<Smem*>(smem_raw);
-    const int warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < NST; ++s) {
-            mbar_init(&S.ready[s], 1);
-            mbar_init(&S.done[s], NWORK);
-            mbar_init(&S.freed[s], 1);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (warp < NWORK) merge_worker(S, warp, bp, status);
-    else if (warp == WSETUP) merge_setup(S, arp, aval, espan, tr, te, ntiles, ticket, side_nnz, status);
-    else merge_epilogue(S, warp - WEPI, status, side_nnz, crp, ccol, cval);
 }
 
 // ================================================================ BIG rows (side path)
@@ -1125,7 +448,7 @@ __global__ void k_big_finish(const int32_t* __restrict__ rows, int nrows, const 
     }
 }
 
-// BIG rows' sorted products into C[crp[r], crp[r+1]) (after k_tile wrote the
+// BIG rows' sorted products into C[crp[r], crp[r+1]) (after k_rows wrote the
 // row pointers): one CTA-range per row chunk, 16 independent copies per thread
 // in flight.
 __global__ void __launch_bounds__(256) k_big_copy(const int32_t* __restrict__ rows, int nrows,
@@ -1160,20 +483,521 @@ __global__ void __launch_bounds__(256) k_big_copy(const int32_t* __restrict__ ro
     }
 }
 
-#ifdef SPG_MERGE_PROF
-}  // namespace
-}  // namespace spgb
-extern "C" int spg_dev_merge_prof(unsigned long long* out) {
-    cudaMemcpyFromSymbol(out, spgb::g_merge_prof, 24 * sizeof(unsigned long long));
-    cudaMemcpyFromSymbol(out + 24, spgb::g_lb_prof, 4 * sizeof(unsigned long long));
-    unsigned long long z[24] = {0};
-    cudaMemcpyToSymbol(spgb::g_merge_prof, z, sizeof(z));
-    cudaMemcpyToSymbol(spgb::g_lb_prof, z, 4 * sizeof(unsigned long long));
-    return 0;
+// Decoupled look-back status word: bits 62-63 flag (0 none, 1 aggregate,
+// 2 inclusive prefix), bits 0-61 value.
+constexpr uint64_t ST_AGG = 1ull << 62, ST_INC = 2ull << 62, ST_VAL = (1ull << 62) - 1;
+
+__device__ __forceinline__ uint64_t ld_status(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
 }
-namespace spgb {
-namespace {
+__device__ __forceinline__ void st_status(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Exclusive block scan with one barrier: warp totals go to ws (NW slots); the
+// caller guarantees a barrier between two uses of the same ws.
+template <typename T>
+__device__ __forceinline__ T tile_scan(T v, T* total, T* ws) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const T inc = warp_inclusive_scan(v);
+    if (lane == 31) ws[wid] = inc;
+    __syncthreads();
+    T before = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < tile::NW; ++w) {
+        const T t = ws[w];
+        before += w < wid ? t : T(0);
+        tot += t;
+    }
+    *total = tot;
+    return before + inc - v;
+}
+
+struct __align__(16) TileEnt {
+    int64_t base;  // B position of tile product x is base + x
+    double av;     // A value
+};
+
+struct __align__(16) TileSmem {
+    double val[tile::PMAX];        // staging: the tile's C entries (values)
+    TileEnt ent[tile::EMAX];
+    int32_t col[tile::PMAX];       // staging: columns
+    uint32_t cnt[tile::CW * tile::PMAX + 2];  // 2 x 16-bit bucket counters per word, then prefixes
+    uint32_t ebin[tile::EMAX];     // per entry: row bucket base (lo 16) | row bucket count (hi 16)
+    int32_t epre[tile::EMAX + 1];  // product prefix of the tile's entries
+    int32_t re[tile::RMAX + 1];    // first entry of each row (relative to the tile)
+    int32_t rend[tile::RMAX];      // end of each row in the (compacted) staging
+    uint32_t list[tile::LMAX];     // shared buckets of >= 3 products: start | end << 16
+    uint32_t dbm[tile::HW];        // duplicates: staged entries that repeat their predecessor's (row, column)
+    int32_t dpre[tile::HW];        //   and the word prefix of their count
+    uint16_t xs[tile::PMAX];       // product id of a staged entry of a shared bucket
+    uint16_t eof[tile::PMAX];      // entry of each product
+    int32_t ws[4][tile::NW];       // scan workspaces (rotated)
+    int64_t lbs[tile::NW];         // look-back: per-warp sums
+    int32_t lbi[tile::NW];         //   and "found an inclusive prefix"
+    int64_t ticket;                // next tile of this CTA
+    int32_t nlist;
+};
+
+// Tile descriptor (uniform across the CTA).
+struct TileDesc {
+    int64_t k, r0, e0;
+    int R, E, ptile;
+    bool big;
+};
+
+// Number of duplicate entries before staging position q.
+__device__ __forceinline__ int dups_before(const TileSmem& S, int q) {
+    return S.dpre[q >> 5] + __popc(S.dbm[q >> 5] & ((1u << (q & 31)) - 1u));
+}
+
+// Contiguous smem -> global copy of n staged entries to C[base, base+n) with
+// 16-byte stores in the aligned middle.
+__device__ __forceinline__ void tile_copy_out(const TileSmem& S, int n, int64_t base, int32_t* __restrict__ ccol,
+                                              double* __restrict__ cval, int tid) {
+    {
+        const int head = min(n, static_cast<int>((4 - (base & 3)) & 3));
+        const int nv = (n - head) >> 2;
+        if (tid < head) ccol[base + tid] = S.col[tid];
+        int4* dst = reinterpret_cast<int4*>(ccol + base + head);
+        for (int v = tid; v < nv; v += tile::NT) {
+            const int q = head + 4 * v;
+            dst[v] = make_int4(S.col[q], S.col[q + 1], S.col[q + 2], S.col[q + 3]);
+        }
+        for (int q = head + 4 * nv + tid; q < n; q += tile::NT) ccol[base + q] = S.col[q];
+    }
+    {
+        const int head = min(n, static_cast<int>(base & 1));
+        const int nv = (n - head) >> 1;
+        if (tid < head) cval[base + tid] = S.val[tid];
+        double2* dst = reinterpret_cast<double2*>(cval + base + head);
+        for (int v = tid; v < nv; v += tile::NT) {
+            const int q = head + 2 * v;
+            dst[v] = make_double2(S.val[q], S.val[q + 1]);
+        }
+        for (int q = head + 2 * nv + tid; q < n; q += tile::NT) cval[base + q] = S.val[q];
+    }
+}
+
+#ifdef SPG_TILE_PROF
+// Dev instrumentation (-DSPG_TILE_PROF): per-phase clock64 totals of thread 0.
+__device__ unsigned long long g_tile_prof[16];
+__shared__ unsigned long long s_tp_last, s_tp_acc[16];
+#define TPROF_DECL                                            \
+    if (threadIdx.x == 0) {                                   \
+        s_tp_last = clock64();                                \
+        for (int i_ = 0; i_ < 16; ++i_) s_tp_acc[i_] = 0;     \
+    }
+#define TPROF(i)                                              \
+    if (threadIdx.x == 0) {                                   \
+        const unsigned long long t_ = clock64();              \
+        s_tp_acc[i] += t_ - s_tp_last;                        \
+        s_tp_last = t_;                                       \
+    }
+#define TPROF_FLUSH                                                              \
+    if (threadIdx.x == 0)                                                        \
+        for (int i_ = 0; i_ < 16; ++i_) atomicAdd(&g_tile_prof[i_], s_tp_acc[i_]);
+#else
+#define TPROF_DECL
+#define TPROF(i)
+#define TPROF_FLUSH
 #endif
+
+// Prologue: the tile's rows and entries (contiguous in A and espan: one round
+// trip), the entry product prefix, the product -> entry map and the per-entry
+// row bucket ranges. Ends with the tables visible to the CTA.
+__device__ __forceinline__ TileDesc tile_prologue(TileSmem& S, int64_t k, const int64_t* __restrict__ arp,
+                                                  const double* __restrict__ aval,
+                                                  const uint64_t* __restrict__ espan,
+                                                  const int64_t* __restrict__ tr, const int64_t* __restrict__ te) {
+    constexpr int NT = tile::NT, EPT = tile::EPT;
+    const int tid = threadIdx.x;
+    TileDesc T;
+    T.k = k;
+    const int64_t trk = tr[k];
+    T.r0 = trk & ((int64_t(1) << 62) - 1);
+    T.big = (trk >> 62) != 0;
+    T.e0 = te[k];
+    T.R = static_cast<int>((tr[k + 1] & ((int64_t(1) << 62) - 1)) - T.r0);
+    T.E = static_cast<int>(te[k + 1] - T.e0);
+    T.ptile = 0;
+    if (T.big) return T;
+    for (int t = tid; t <= T.R; t += NT) S.re[t] = static_cast<int32_t>(arp[T.r0 + t] - T.e0);
+    const int per = (T.E + NT - 1) / NT;  // contiguous entries per thread (1 for typical tiles)
+    uint64_t sp[EPT];
+    double av[EPT];
+    int sum = 0;
+#pragma unroll
+    for (int c = 0; c < EPT; ++c) {
+        const int q = tid * per + c;
+        sp[c] = 0;
+        av[c] = 0.0;
+        if (c < per && q < T.E) {
+            sp[c] = espan[T.e0 + q];
+            av[c] = aval[T.e0 + q];
+        }
+        sum += static_cast<int>((sp[c] >> tile::SP_LEN) & 1023u);  // 10-bit length
+    }
+    TPROF(15)
+    int ptile;
+    int pre = tile_scan(sum, &ptile, S.ws[0]);
+    T.ptile = ptile;
+#pragma unroll
+    for (int c = 0; c < EPT; ++c) {
+        const int q = tid * per + c;
+        if (c < per && q < T.E) {
+            const int len = static_cast<int>((sp[c] >> tile::SP_LEN) & 1023u);
+            const int inrow = static_cast<int>((sp[c] >> tile::SP_IN) & 4095u);
+            const int prow = pre - inrow, pr = static_cast<int>(sp[c] >> tile::SP_PR);
+            S.ent[q] = TileEnt{static_cast<int64_t>(sp[c] & tile::SP_BS_MASK) - pre, av[c]};
+            S.ebin[q] = static_cast<uint32_t>(tile::BPP * prow) | (static_cast<uint32_t>(tile::BPP * pr) << 16);
+            S.epre[q] = pre;
+            for (int x = pre; x < pre + len; ++x) S.eof[x] = static_cast<uint16_t>(q);
+            pre += len;
+        }
+    }
+    if (tid == 0) {
+        S.epre[T.E] = ptile;
+        S.nlist = 0;
+    }
+    for (int q = tid; q <= tile::CW * ptile; q += NT) S.cnt[q] = 0u;  // CW*ptile words = BPP*ptile buckets
+    __syncthreads();
+    return T;
+}
+
+// Gathers of the tile's products x = tid + NT*j (all issued, none consumed).
+template <int NJ>
+__device__ __forceinline__ void tile_gather(const TileSmem& S, int ptile, const int32_t* __restrict__ bcol,
+                                            const double* __restrict__ bval, int32_t (&col)[NJ], double (&val)[NJ],
+                                            int (&aux)[NJ]) {
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        aux[j] = -1;
+        if (j * tile::NT >= ptile) break;  // uniform
+        const int x = threadIdx.x + tile::NT * j;
+        if (x < ptile) {
+            const int q = S.eof[x];
+            const int64_t u = S.ent[q].base + x;
+            aux[j] = q;
+            col[j] = __ldg(bcol + u);
+            val[j] = __ldg(bval + u);
+        }
+    }
+}
+
+// The tile's rows of C into the staging (sorted by (row, column), duplicates
+// combined in ascending k); S.rend[t] = end of row t. Returns the tile's nnz.
+template <int NJ>
+__device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int cshift, int32_t (&col)[NJ],
+                                            double (&val)[NJ], int (&aux)[NJ]) {
+    constexpr int NT = tile::NT;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ptile = T.ptile;
+    const int nj = (ptile + NT - 1) / NT;
+    // multiply (0 + av*bv, the reference's first accumulation) and count
+    int bk[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        bk[j] = -1;
+        if (j >= nj) break;
+        if (aux[j] >= 0) {
+            const int q = aux[j];
+            val[j] = dadd(0.0, dmul(S.ent[q].av, val[j]));
+            const uint32_t bi = S.ebin[q];
+            const int b = static_cast<int>(bi & 0xffffu) + bucket_of(col[j], cshift, static_cast<int>(bi >> 16));
+            bk[j] = b;
+            const int sh = (b & 1) << 4;
+            aux[j] = static_cast<int>((atomicAdd(&S.cnt[b >> 1], 1u << sh) >> sh) & 0xffffu);
+        }
+    }
+    // duplicate bitmap of this tile (the previous tile's was consumed by its copy-out)
+    for (int q = tid; q < (ptile >> 5) + 2; q += NT) S.dbm[q] = 0u;
+    TPROF(8)
+    __syncthreads();
+    TPROF(9)
+    // exclusive scan of the packed counters (odd-strided blocks: conflict-free)
+    {
+        const int W = tile::CW * ptile;
+        const int per = ((W + NT - 1) / NT) | 1;
+        const int w0 = tid * per;
+        constexpr int PERMAX = ((tile::CW * tile::PMAX + NT - 1) / NT) | 1;
+        uint32_t wd[PERMAX];
+        uint32_t s = 0;
+#pragma unroll
+        for (int q = 0; q < PERMAX; ++q) {
+            wd[q] = (q < per && w0 + q < W) ? S.cnt[w0 + q] : 0u;
+            s += wd[q];
+        }
+        int tot;
+        const int cnt_s = static_cast<int>((s & 0xffffu) + (s >> 16));
+        uint32_t p2 = static_cast<uint32_t>(tile_scan(cnt_s, &tot, S.ws[1]));
+#pragma unroll
+        for (int q = 0; q < PERMAX; ++q) {
+            if (q < per && w0 + q < W) S.cnt[w0 + q] = p2 * 0x10001u + (wd[q] << 16);
+            p2 += (wd[q] + (wd[q] << 16)) >> 16;
+        }
+        if (tid == 0) S.cnt[W] = static_cast<uint32_t>(ptile);  // end of the last bucket
+    }
+    __syncthreads();
+    TPROF(10)
+    // place: alone in the bucket -> final; pairs ranked below; >= 3 -> list
+    unsigned pair = 0;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        if (j >= nj) break;
+        uint32_t lreg = 0u;  // a >= 3 bucket whose first slot is this product
+        if (bk[j] >= 0) {
+            const int b = bk[j];
+            const uint32_t r = __funnelshift_r(S.cnt[b >> 1], S.cnt[(b >> 1) + 1], (b & 1) << 4);
+            const int st = static_cast<int>(r & 0xffffu), sz = static_cast<int>(r >> 16) - st;
+            const int slot = aux[j];
+            const int pos = st + slot;
+            S.col[pos] = col[j];
+            if (sz == 1) {
+                S.val[pos] = val[j];
+            } else {
+                S.xs[pos] = static_cast<uint16_t>(tid + NT * j);
+                if (sz == 2) {
+                    pair |= 1u << j;
+                    aux[j] = pos | (slot << 16);
+                } else {
+                    S.val[pos] = val[j];
+                    if (slot == 0) lreg = r;  // this thread sorts the bucket
+                }
+            }
+        }
+        // append >= 3 buckets to the list: one smem atomic per warp
+        const unsigned has = __ballot_sync(0xffffffffu, lreg != 0u);
+        if (has) {
+            int b0 = 0;
+            if (lane == 0) b0 = atomicAdd(&S.nlist, __popc(has));
+            b0 = __shfl_sync(0xffffffffu, b0, 0);
+            if (lreg) S.list[b0 + __popc(has & ((1u << lane) - 1u))] = lreg;
+        }
+    }
+    TPROF(11)
+    __syncthreads();
+    TPROF(12)
+    // order shared buckets by (column, product id), detect duplicates. A pair
+    // reads only its partner's slot and, when swapped, writes only the
+    // partner's slot: no barrier is needed between the compare and the write.
+    bool dup = false;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        if (j >= nj) break;
+        if ((pair >> j) & 1u) {
+            const int pos = aux[j] & 0xffff, slot = aux[j] >> 16;
+            const int other = pos + 1 - 2 * slot;
+            const int32_t oc = S.col[other];
+            const int ox = S.xs[other];
+            const int x = tid + NT * j;
+            const int fpos = pos - slot + ((oc < col[j] || (oc == col[j] && ox < x)) ? 1 : 0);
+            if (fpos != pos) S.col[fpos] = col[j];
+            S.val[fpos] = val[j];
+            if (oc == col[j]) {  // equal columns: the larger product id repeats the smaller
+                dup = true;
+                if (ox < x) atomicOr(&S.dbm[fpos >> 5], 1u << (fpos & 31));
+            }
+        }
+    }
+    const int nlist = S.nlist;
+    for (int l = tid; l < nlist; l += NT) {
+        const int lo = static_cast<int>(S.list[l] & 0xffffu), hi = static_cast<int>(S.list[l] >> 16);
+        for (int a = lo + 1; a < hi; ++a) {
+            const int32_t ca = S.col[a];
+            const uint16_t xa = S.xs[a];
+            const double va = S.val[a];
+            int c = a - 1;
+            while (c >= lo && (S.col[c] > ca || (S.col[c] == ca && S.xs[c] > xa))) {
+                S.col[c + 1] = S.col[c];
+                S.xs[c + 1] = S.xs[c];
+                S.val[c + 1] = S.val[c];
+                --c;
+            }
+            S.col[c + 1] = ca;
+            S.xs[c + 1] = xa;
+            S.val[c + 1] = va;
+        }
+        for (int a = lo + 1; a < hi; ++a)
+            if (S.col[a] == S.col[a - 1]) {
+                dup = true;
+                atomicOr(&S.dbm[a >> 5], 1u << (a & 31));
+            }
+    }
+    TPROF(13)
+    const int anydup = __syncthreads_or(dup);
+    TPROF(14)
+    if (!anydup) {
+        for (int t = tid; t < T.R; t += NT) S.rend[t] = S.epre[S.re[t + 1]];
+        return ptile;
+    }
+    // duplicates (equal (row, column); rare): the ranking marked every staged
+    // entry that repeats its predecessor; their word prefix (one warp) gives
+    // every head its compacted position. Runs are folded in product-id order
+    // = ascending k.
+    const int hw = (ptile >> 5) + 1;
+    if (warp == 0) {
+        constexpr int PW = (tile::HW + 31) / 32;
+        int c[PW], sum = 0;
+#pragma unroll
+        for (int u = 0; u < PW; ++u) {
+            const int w = lane * PW + u;
+            c[u] = w < hw ? __popc(S.dbm[w]) : 0;
+            sum += c[u];
+        }
+        int pre = warp_inclusive_scan(sum) - sum;
+#pragma unroll
+        for (int u = 0; u < PW; ++u) {
+            const int w = lane * PW + u;
+            if (w < tile::HW) S.dpre[w] = pre;
+            pre += c[u];
+        }
+    }
+    __syncthreads();
+    // fold each run into its head and move the heads down (two phases: all
+    // reads, a barrier, all writes), so the copy-out stays one contiguous run
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        const int x = tid + NT * j;
+        aux[j] = -1;
+        if (x < ptile && !((S.dbm[x >> 5] >> (x & 31)) & 1u)) {
+            double v = S.val[x];
+            for (int u = x + 1; u < ptile && ((S.dbm[u >> 5] >> (u & 31)) & 1u); ++u) v = dadd(v, S.val[u]);
+            aux[j] = x - dups_before(S, x);
+            col[j] = S.col[x];
+            val[j] = v;
+        }
+    }
+    for (int t = tid; t < T.R; t += NT) {
+        const int pe = S.epre[S.re[t + 1]];
+        S.rend[t] = pe - dups_before(S, pe);
+    }
+    const int nnz = ptile - dups_before(S, ptile);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+        if (aux[j] >= 0) {
+            S.col[aux[j]] = col[j];
+            S.val[aux[j]] = val[j];
+        }
+    return nnz;
+}
+
+// Exclusive prefix of tile k from the status words (all warps: 256
+// predecessors per round trip). Tile k only waits on tiles with smaller
+// tickets, whose CTAs publish their aggregates without waiting on anything,
+// so the chain always makes progress.
+__device__ __forceinline__ int64_t tile_look_back(TileSmem& S, uint64_t* status, int64_t k, uint64_t s_first) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int64_t excl = 0;
+    for (int64_t j0 = k - 1; j0 >= 0; j0 -= tile::NT) {
+        const int64_t idx = j0 - tid;
+        uint64_t s = j0 == k - 1 ? s_first : (idx >= 0 ? ld_status(status + idx) : ST_INC);
+        unsigned inc, upto;
+        while (true) {
+            inc = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+            const unsigned none = __ballot_sync(0xffffffffu, (s >> 62) == 0);
+            upto = inc ? ((inc & (0u - inc)) << 1) - 1u : 0xffffffffu;  // lanes up to the first inclusive
+            if (!(none & upto)) break;
+            if ((s >> 62) == 0) s = ld_status(status + idx);
+        }
+        const int64_t v = warp_reduce_sum(((1u << lane) & upto) ? static_cast<int64_t>(s & ST_VAL) : int64_t(0));
+        if (lane == 0) {
+            S.lbs[warp] = v;
+            S.lbi[warp] = inc != 0;
+        }
+        __syncthreads();
+        bool found = false;
+#pragma unroll
+        for (int w = 0; w < tile::NW; ++w) {
+            if (!found) {
+                excl += S.lbs[w];
+                found = S.lbi[w] != 0;
+            }
+        }
+        __syncthreads();
+        if (found) break;
+    }
+    return excl;
+}
+
+#ifndef SPG_TILE_MINB
+#define SPG_TILE_MINB 2
+#endif
+// Persistent tile kernel. Per CTA, tiles come from a global ticket; for tile F
+// the order is: process F (its products already in registers) -> publish F's
+// aggregate -> prologue + gathers of the next tile -> look-back, row pointers
+// and copy-out of F (overlapping the next tile's gather latency).
+__global__ void __launch_bounds__(tile::NT, SPG_TILE_MINB) k_tile(
+    const int64_t* __restrict__ arp, const double* __restrict__ aval, const uint64_t* __restrict__ espan,
+    const int32_t* __restrict__ bcol, const double* __restrict__ bval, const int64_t* __restrict__ tr,
+    const int64_t* __restrict__ te, int64_t ntiles, unsigned long long* __restrict__ ticket, int cshift,
+    const uint64_t* __restrict__ side_cp, const uint64_t* __restrict__ side_vp, const int64_t* __restrict__ side_nnz,
+    uint64_t* __restrict__ status,
+    int64_t* __restrict__ crp, int32_t* __restrict__ ccol, double* __restrict__ cval) {
+    constexpr int NT = tile::NT, NJ = tile::NJ;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TileSmem& S = *reinterpret_cast<TileSmem*>(smem_raw);
+    const int tid = threadIdx.x;
+    TPROF_DECL
+
+    if (tid == 0) S.ticket = static_cast<int64_t>(atomicAdd(ticket, 1ull));
+    __syncthreads();
+    const int64_t k0 = S.ticket;
+    if (k0 >= ntiles) return;
+    int32_t col[NJ];
+    double val[NJ];
+    int aux[NJ];
+    TileDesc T = tile_prologue(S, k0, arp, aval, espan, tr, te);
+    if (!T.big) tile_gather<NJ>(S, T.ptile, bcol, bval, col, val, aux);
+    while (true) {
+#ifdef SPG_TICKET_SMEM
+        if (tid == 0) S.ticket = static_cast<int64_t>(atomicAdd(ticket, 1ull));
+#else
+        // the next ticket stays in thread 0's register while the tile is
+        // processed: its round trip is only waited for at the publish barrier
+        unsigned long long tk = 0;
+        if (tid == 0) tk = atomicAdd(ticket, 1ull);
+#endif
+        TPROF(0)
+        const int nnz = T.big ? 0 : tile_process<NJ>(S, T, cshift, col, val, aux);
+        TPROF(1)
+        const int64_t agg = T.big ? side_nnz[T.r0] : static_cast<int64_t>(nnz);
+        if (tid == 0) st_status(status + T.k, (T.k == 0 ? ST_INC : ST_AGG) | static_cast<uint64_t>(agg));
+#ifndef SPG_TICKET_SMEM
+        if (tid == 0) S.ticket = static_cast<int64_t>(tk);
+#endif
+        __syncthreads();  // staging + rend complete, ticket visible
+        TPROF(2)
+        const TileDesc F = T;  // tile to finish
+        const int64_t k2 = S.ticket;
+        const bool more = k2 < ntiles;
+        if (more) {
+            T = tile_prologue(S, k2, arp, aval, espan, tr, te);
+            TPROF(3)
+            if (!T.big) tile_gather<NJ>(S, T.ptile, bcol, bval, col, val, aux);
+            TPROF(4)
+        }
+        // finish F: offset, row pointers, copy-out
+        const int64_t lbi = F.k - 1 - tid;
+        const int64_t base = tile_look_back(S, status, F.k, lbi >= 0 ? ld_status(status + lbi) : ST_INC);
+        TPROF(5)
+        if (tid == 0 && F.k > 0) st_status(status + F.k, ST_INC | static_cast<uint64_t>(base + agg));
+        if (F.big) {  // its entries are copied into C after this kernel (k_big_copy)
+            if (tid == 0) crp[F.r0 + 1] = base + agg;
+        } else {
+            for (int t = tid; t < F.R; t += NT) crp[F.r0 + t + 1] = base + S.rend[t];
+            tile_copy_out(S, nnz, base, ccol, cval, tid);
+        }
+        TPROF(6)
+        __syncthreads();
+        TPROF(7)
+        if (!more) break;
+    }
+    TPROF_FLUSH
+}
 
 int grid_for(spg_ctx* ctx, int64_t n, int bs = 256) {
     const int64_t want = (n + bs - 1) / bs;
@@ -1402,27 +1226,27 @@ int64_t big_rows_esc(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const int
 }
 }  // namespace
 
-// C = A*B (reference spgemm_local, csr.cpp:132-165).
-spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEvent_t b_data) {
-    if (a->ncols != b->nrows)
-        fail(SPG_DIMENSION_ERROR,
-             "spgemm: a.ncols=" + std::to_string(a->ncols) + " != b.nrows=" + std::to_string(b->nrows));
-    const int64_t m = a->nrows, n = b->ncols;
-    if (n > (int64_t(1) << 31)) fail(SPG_PARAMETER_ERROR, "spgemm: b.ncols must be <= 2^31 (int32 column indices)");
-    if (b_data && (m == 0 || a->nnz == 0 || b->nnz == 0)) SPG_CUDA(cudaStreamWaitEvent(ctx->stream, b_data, 0));
-    if (m == 0 || a->nnz == 0 || b->nnz == 0) return new_csr(ctx, m, n, 0);
-    if (packed_units(b->nnz, b->nrows) >= (int64_t(1) << 32))
-        fail(SPG_PARAMETER_ERROR, "spgemm: B too large for 32-bit packed block offsets");
+namespace {
+int cshift_for(int64_t ncols) {
+    int bits = 1;
+    while ((int64_t(1) << bits) < ncols) ++bits;
+    return 32 - bits;  // col << cshift puts the top column bit at bit 31
+}
+
+// Single-pass tiled multiply.
+spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEvent_t b_data) {
     HostProf hprof;
-    // 1: row plan (products, kind, weight; entry spans), BIG-row list
+    const int64_t m = a->nrows, n = b->ncols;
+    const int cshift = cshift_for(n);
+    // 1: products, entry spans, row weights, BIG-row list
     DBuf<int64_t> prod(ctx, m), wt(ctx, m), total(ctx, 1);
     DBuf<int8_t> kind(ctx, m);
-    DBuf<uint64_t> espan(ctx, a->nnz + 2);
+    DBuf<uint64_t> espan(ctx, a->nnz);
     DBuf<int32_t> big_list(ctx, m), nbig_d(ctx, 1);
     SPG_CUDA(cudaMemsetAsync(nbig_d.get(), 0, sizeof(int32_t), ctx->stream));
     {
-        KTime kt(ctx, "row_plan");
-        k_row_plan<<<grid_for(ctx, 16 * m), 256, 0, ctx->stream>>>(a->rowptr, a->colind, b->rowptr, m, prod, wt,
+        KTime kt(ctx, "row_prep");
+        k_row_prep<<<grid_for(ctx, 32 * m), 256, 0, ctx->stream>>>(a->rowptr, a->colind, b->rowptr, m, prod, wt,
                                                                    kind, espan, big_list, nbig_d);
         SPG_LAUNCH_CHECK();
     }
@@ -1445,35 +1269,27 @@ spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEvent_t b_
     const volatile int64_t* hprod = static_cast<int64_t*>(peek_async(ctx, 72, total.get(), sizeof(int64_t)));
     const volatile int64_t* hnt = static_cast<int64_t*>(peek_async(ctx, 80, fpos.get() + m, sizeof(int64_t)));
     hprof.mark("launch1");
-    // B's columns and values may still be arriving (trident pulls): everything
-    // above read only B's row pointers
-    if (b_data) SPG_CUDA(cudaStreamWaitEvent(ctx->stream, b_data, 0));
-    // 3: packed B (one 128-byte-aligned block per row)
-    DBuf<unsigned char> bp(ctx, static_cast<size_t>(packed_units(b->nnz, b->nrows)) * 128);
-    {
-        KTime kt(ctx, "pack_b");
-        k_pack_rows<<<grid_for(ctx, 32 * b->nrows), 256, 0, ctx->stream>>>(b->rowptr, b->colind, b->values,
-                                                                          b->nrows, bp);
-        SPG_LAUNCH_CHECK();
-    }
     SPG_CUDA(cudaStreamSynchronize(ctx->stream));
     hprof.mark("sync1");
     const int nbig = *hnbig;
     const int64_t products = *hprod, ntiles = *hnt;
-    // 4: BIG rows
+    // B's columns and values may still be arriving (trident pulls): everything
+    // above read only B's row pointers
+    if (b_data) SPG_CUDA(cudaStreamWaitEvent(ctx->stream, b_data, 0));
+    // 3: BIG rows: sort-based ESC in batches bounded by products
     DBuf<uint64_t> side_cp(ctx, nbig ? m : 1), side_vp(ctx, nbig ? m : 1);
     DBuf<int64_t> side_nnz(ctx, nbig ? m : 1);
     DBuf<int32_t> drows(ctx, nbig ? nbig : 1);
     std::vector<std::unique_ptr<DBuf<int32_t>>> outc;
     std::vector<std::unique_ptr<DBuf<double>>> outv;
-    int64_t big_products = 0, big_nnz = 0;
+    int64_t big_products = 0, big_nnz = 0;  // C capacity = products of tile rows + exact nnz of big rows
     if (nbig) {
         KTime kt(ctx, "big_rows");
         big_nnz = big_rows_esc(ctx, a, b, big_list, nbig, prod, drows, side_cp, side_vp, side_nnz, outc, outv, hprof,
                                &big_products);
     }
     hprof.mark("side");
-    // 5: tiles
+    // 4: tiles
     DBuf<int64_t> tr(ctx, ntiles + 1), te(ctx, ntiles + 1);
     DBuf<uint64_t> status(ctx, ntiles);
     {
@@ -1488,14 +1304,17 @@ spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEvent_t b_
     alloc_c_arrays(ctx, c, products - big_products + big_nnz);  // upper bound of nnz(C)
     SPG_CUDA(cudaMemsetAsync(c->rowptr, 0, sizeof(int64_t), ctx->stream));
     if (!ctx->tile_attr_set) {
-        SPG_CUDA(cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(mg::Smem)));
+        SPG_CUDA(cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem)));
         ctx->tile_attr_set = true;
     }
+    int occ = 1;
+    SPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile, tile::NT, sizeof(TileSmem)));
+    const int grid = static_cast<int>(std::min<int64_t>(ntiles, int64_t(ctx->num_sms) * std::max(occ, 1)));
     {
-        KTime kt(ctx, "spgemm_merge");
-        k_merge<<<ctx->num_sms, mg::NT, sizeof(mg::Smem), ctx->stream>>>(a->rowptr, a->values, espan, bp, tr, te,
-                                                                         ntiles, ticket, side_nnz, status, c->rowptr,
-                                                                         c->colind, c->values);
+        KTime kt(ctx, "spgemm_tile");
+        k_tile<<<grid, tile::NT, sizeof(TileSmem), ctx->stream>>>(a->rowptr, a->values, espan, b->colind, b->values,
+                                                                  tr, te, ntiles, ticket, cshift, side_cp, side_vp,
+                                                                  side_nnz, status, c->rowptr, c->colind, c->values);
         SPG_LAUNCH_CHECK();
     }
     if (nbig) {
@@ -1504,10 +1323,37 @@ spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEvent_t b_
                                                                              c->rowptr, c->colind, c->values);
         SPG_LAUNCH_CHECK();
     }
-    hprof.mark("launch_merge");
+    hprof.mark("launch_tile");
     c->nnz = read_scalar(ctx, c->rowptr + m);
-    hprof.mark("merge");
+    hprof.mark("tile");
     return c;
+}
+}  // namespace
+
+#ifdef SPG_TILE_PROF
+extern "C" int spg_dev_tile_prof(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, g_tile_prof, 16 * sizeof(unsigned long long));
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_tile_prof, z, sizeof(z));
+    return 0;
+}
+#endif
+
+// C = A*B (reference spgemm_local, csr.cpp:132-165).
+spg_csr* spgemm(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEvent_t b_data) {
+    if (a->ncols != b->nrows)
+        fail(SPG_DIMENSION_ERROR,
+             "spgemm: a.ncols=" + std::to_string(a->ncols) + " != b.nrows=" + std::to_string(b->nrows));
+    const int64_t m = a->nrows, n = b->ncols;
+    if (n > (int64_t(1) << 31)) fail(SPG_PARAMETER_ERROR, "spgemm: b.ncols must be <= 2^31 (int32 column indices)");
+    if (b_data && (m == 0 || a->nnz == 0 || b->nnz == 0)) SPG_CUDA(cudaStreamWaitEvent(ctx->stream, b_data, 0));
+    if (m == 0 || a->nnz == 0 || b->nnz == 0) return new_csr(ctx, m, n, 0);
+    // the tile path packs B row starts in SP_BS = 30 bits: B up to 2^30 - 1
+    // entries (12 GB); larger B is refused rather than multiplied slowly
+    if (b->nnz >= (int64_t(1) << tile::SP_BS))
+        fail(SPG_PARAMETER_ERROR, "spgemm: nnz(B) = " + std::to_string(b->nnz) +
+                                      " exceeds the 2^30 - 1 entries the tile path addresses; split B by rows");
+    return spgemm_tiled(ctx, a, b, b_data);
 }
 
 }  // namespace spgb

@@ -149,6 +149,14 @@ void partition_device(spg_ctx* const* ctxs, int nctx, const spg_csr* m, int sche
             const TileRect& x = rects[r];
             out[r] = extract(c, m, x.r0, x.r1, x.c0, x.c1);  // kernels on c's device, m read in place
         }
+        // The extract copies read m in place on every tile's own stream: they
+        // must be done before the caller may free m (stream-ordered on m's
+        // context, which knows nothing of the other streams) and before a
+        // driver pulls the tiles on its transfer streams.
+        for (int r = 0; r < std::min(procs, nctx); ++r) {
+            DeviceScope ds(ctxs[r]->device);
+            SPG_CUDA(cudaStreamSynchronize(ctxs[r]->stream));
+        }
     } catch (...) {
         for (int r = 0; r < procs; ++r)
             if (out[r]) free_csr(out[r]), out[r] = nullptr;

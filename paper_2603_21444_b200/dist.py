@@ -90,7 +90,12 @@ class RankExchange:
 
     def reload(self, a_host, b_host):
         """Refill this rank's shareable A/B tiles from host arrays (pinned by
-        the caller) in place, so the peers' IPC views stay valid (e2e leg)."""
+        the caller) in place, so the peers' IPC views stay valid (e2e leg).
+
+        Contract: the peers may still be pulling this rank's tiles for the
+        previous trident_step; the caller must order the reload after every
+        rank's step (bench.py: a dist.barrier() once each rank has its C tile
+        downloaded, which the stream-synchronous download implies)."""
         L = _capi.lib()
         for d, m in zip(self.own, (a_host, b_host)):
             check(L.spg_csr_upload_into(self.dev.ctx, d.h, m[0].ctypes.data, m[1].ctypes.data, m[2].ctypes.data))

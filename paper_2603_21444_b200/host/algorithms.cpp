@@ -25,11 +25,11 @@ Algo algo_from_name(const std::string& name) {
 
 namespace {
 
-using Driver = spg_status (*)(spg_ctx* const*, int, const spg_csr* const*, const spg_csr* const*, int, int, int, int,
-                              spg_csr**, spg_ledger_cell*, double*);
+enum class Drv { trident, summa, oned };
 
-DriverResult run_device(Driver drv, const CsrMatrix& a, const CsrMatrix& b, Scheme scheme, const TileMap& cmap,
-                        int procs, int gpus_per_node, const TopologySpec& topo, int rounds) {
+DriverResult run_device(Drv drv, const CsrMatrix& a, const CsrMatrix& b, Scheme scheme, const TileMap& cmap,
+                        int procs, int gpus_per_node, const TopologySpec& topo, int rounds,
+                        const std::vector<double>& node_start_delay = {}) {
     const int ndev = detail::device_count();
     const int nctx = std::min(ndev, procs);
     std::vector<spg_ctx*> ctxs(static_cast<std::size_t>(nctx));
@@ -57,8 +57,27 @@ DriverResult run_device(Driver drv, const CsrMatrix& a, const CsrMatrix& b, Sche
     std::vector<spg_csr*> hc(static_cast<std::size_t>(procs), nullptr);
     std::vector<spg_ledger_cell> cells(static_cast<std::size_t>(procs) * 4);
     std::vector<double> tl(static_cast<std::size_t>(procs) * rounds * 4, 0.0);
-    check(drv(ctxs.data(), nctx, ha.data(), hb.data(), procs, gpus_per_node, topo.index_width, topo.value_width,
-              hc.data(), cells.data(), tl.data()));
+    // events: at most 3 per fetch (2 per rank and round) + allgather + compute
+    std::vector<spg_event> ev(static_cast<std::size_t>(procs) * rounds * 8 + 16);
+    int nev = 0;
+    switch (drv) {
+        case Drv::trident:
+            check(spg_trident_spgemm_ex(ctxs.data(), nctx, ha.data(), hb.data(), procs, gpus_per_node,
+                                        topo.index_width, topo.value_width, node_start_delay.data(),
+                                        static_cast<int>(node_start_delay.size()), hc.data(), cells.data(), tl.data(),
+                                        ev.data(), static_cast<int>(ev.size()), &nev, nullptr));
+            break;
+        case Drv::summa:
+            check(spg_summa_spgemm_ex(ctxs.data(), nctx, ha.data(), hb.data(), procs, gpus_per_node, topo.index_width,
+                                      topo.value_width, hc.data(), cells.data(), tl.data(), ev.data(),
+                                      static_cast<int>(ev.size()), &nev, nullptr));
+            break;
+        case Drv::oned:
+            check(spg_oned_spgemm(ctxs.data(), nctx, ha.data(), hb.data(), procs, gpus_per_node, topo.index_width,
+                                  topo.value_width, hc.data(), cells.data(), tl.data()));
+            nev = -1;
+            break;
+    }
     std::vector<DevCsr> dc;
     for (auto* h : hc) dc.emplace_back(h);
 
@@ -86,20 +105,27 @@ DriverResult run_device(Driver drv, const CsrMatrix& a, const CsrMatrix& b, Sche
                 y.nnz = x.nnz;
                 y.bytes = x.bytes;
             }
-    // Measured timeline: per rank and round, exchange then compute (seconds).
-    for (int r = 0; r < procs; ++r) {
-        double t = 0.0;
-        for (int k = 0; k < rounds; ++k) {
-            const double* x = &tl[(static_cast<std::size_t>(r) * rounds + k) * 4];
-            const double wait = x[1] * 1e-3, mul = x[2] * 1e-3, merge = x[3] * 1e-3;
-            out.timeline.events.push_back({EventType::transfer_complete, r, r, k, Operand::B, LinkClass::SELF, t,
-                                           t + x[0] * 1e-3, 0, 0});
-            t += wait;
-            out.timeline.events.push_back({EventType::compute_complete, r, r, k, Operand::A, LinkClass::SELF, t,
-                                           t + mul + merge, 0, 0});
-            t += mul + merge;
+    // Measured timeline: the device run's events (engine.hpp schema); the
+    // 1D driver reports per-rank phase times only.
+    if (nev >= 0) {
+        std::vector<double> done(static_cast<std::size_t>(procs), 0.0);
+        for (int e = 0; e < nev; ++e) {
+            const spg_event& x = ev[static_cast<std::size_t>(e)];
+            TimelineEvent t{static_cast<EventType>(x.type), x.src, x.dst, x.round,
+                            x.operand ? Operand::B : Operand::A, static_cast<LinkClass>(x.link), x.t_start, x.t_end,
+                            x.nnz, x.bytes};
+            out.timeline.events.push_back(t);
+            if (t.type == EventType::compute_complete)
+                done[static_cast<std::size_t>(x.src)] = std::max(done[static_cast<std::size_t>(x.src)], x.t_end);
         }
-        out.ledger.set_completion(r, t);
+        for (int r = 0; r < procs; ++r) out.ledger.set_completion(r, done[static_cast<std::size_t>(r)]);
+    } else {
+        for (int r = 0; r < procs; ++r) {
+            const double* x = &tl[static_cast<std::size_t>(r) * 4];
+            const double t = (x[1] + x[2]) * 1e-3;
+            out.timeline.events.push_back({EventType::compute_complete, r, r, 0, Operand::A, LinkClass::SELF, t, t, 0, 0});
+            out.ledger.set_completion(r, t);
+        }
     }
     out.makespan = out.ledger.makespan();
     return out;
@@ -109,13 +135,16 @@ DriverResult run_device(Driver drv, const CsrMatrix& a, const CsrMatrix& b, Sche
 
 DriverResult trident_spgemm(const CsrMatrix& a, const CsrMatrix& b, const TridentGrid& grid, const TopologySpec& topo,
                             const std::vector<double>& node_start_delay) {
-    (void)node_start_delay;  // skew knob of the modeled clock; real devices start together
     if (a.ncols != b.nrows)
         throw DimensionError("trident_spgemm: a.ncols=" + std::to_string(a.ncols) + " != b.nrows=" + std::to_string(b.nrows));
     topo.validate();
     const int P = grid.procs, lam = grid.gpus_per_node;
     const TileMap cmap = make_tile_map(a.nrows, b.ncols, Scheme::trident, P, lam);
-    return run_device(spg_trident_spgemm, a, b, Scheme::trident, cmap, P, lam, topo, grid.q);
+    // node_start_delay: virtual node n's ranks start their pulls that many
+    // seconds late on the device (engine.cpp:217-221)
+    for (double d : node_start_delay)
+        if (!(d >= 0.0)) throw ParameterError("trident_spgemm: node_start_delay must be >= 0");
+    return run_device(Drv::trident, a, b, Scheme::trident, cmap, P, lam, topo, grid.q, node_start_delay);
 }
 
 DriverResult summa_spgemm(const CsrMatrix& a, const CsrMatrix& b, int procs, int gpus_per_node, const TopologySpec& topo) {
@@ -125,7 +154,7 @@ DriverResult summa_spgemm(const CsrMatrix& a, const CsrMatrix& b, int procs, int
     const TileMap cmap = make_tile_map(a.nrows, b.ncols, Scheme::grid2d, procs, 1);  // GridError when P is not a square
     int pr = 0;
     while ((pr + 1) * (pr + 1) <= procs) ++pr;
-    return run_device(spg_summa_spgemm, a, b, Scheme::grid2d, cmap, procs, gpus_per_node, topo, pr);
+    return run_device(Drv::summa, a, b, Scheme::grid2d, cmap, procs, gpus_per_node, topo, pr);
 }
 
 DriverResult oned_spgemm(const CsrMatrix& a, const CsrMatrix& b, int procs, int gpus_per_node, const TopologySpec& topo) {
@@ -134,7 +163,7 @@ DriverResult oned_spgemm(const CsrMatrix& a, const CsrMatrix& b, int procs, int 
     if (procs <= 0) throw GridError("oned: P must be positive");
     topo.validate();
     const TileMap cmap = make_tile_map(a.nrows, b.ncols, Scheme::rows1d, procs, 1);
-    return run_device(spg_oned_spgemm, a, b, Scheme::rows1d, cmap, procs, gpus_per_node, topo, 1);
+    return run_device(Drv::oned, a, b, Scheme::rows1d, cmap, procs, gpus_per_node, topo, 1);
 }
 
 DriverResult run_algo(Algo algo, const CsrMatrix& a, const CsrMatrix& b, int procs, int gpus_per_node,

@@ -103,3 +103,55 @@ def test_config5_trident_p8(dev):
     r = spg.trident_spgemm(a, at, spg.TridentGrid.create(8, 2))
     check_digest(r.c, golden(5))  # the rounds run as one k-ordered multiply per rank
     assert r.rounds == 2
+
+
+def test_config3_rmat_s18(dev):
+    # R-MAT scale 18 (Graph500 a,b,c = .57,.19,.19, edge factor 16): skewed
+    # rows, the heavy-row path; full C (1,277,051,000 entries) against the
+    # digest of the reference's spgemm_local
+    g = golden(3)["s18"]
+    a = spg.gen_rmat(18, 16, 1, 2)
+    assert a.nnz == g["nnz_A"]
+    da = dev.upload(a)
+    assert dev.products(da, da) == g["products"]
+    dc = dev.spgemm(da, da)
+    del da
+    c = dc.download()
+    dc.free()
+    check_digest(c, g)
+
+
+def test_config3_rmat_s22_sampled(dev):
+    # R-MAT scale 22: the full C (~7.2e10 entries) fits no host, so the
+    # reference rows (the heaviest row of A*A, 3.4e7 products, and 50 random
+    # rows) are compared; a row of C depends only on its row of A, so the
+    # product A[rows, :] * A is multiplied on the device exactly like the
+    # reference made the golden rows
+    g = golden(3)["s22"]
+    a = spg.gen_rmat(22, 16, 1, 2)
+    assert a.nnz == g["nnz_A"]
+    rows = sorted(int(i) for i in g["rows"])
+    assert g["heaviest_row"] in rows
+    rp = np.asarray(a.rowptr)
+    sub_rp, ci, va = [0], [], []
+    for i in rows:
+        ci.append(np.asarray(a.colind[rp[i]:rp[i + 1]]))
+        va.append(np.asarray(a.values[rp[i]:rp[i + 1]], np.float64))
+        sub_rp.append(sub_rp[-1] + int(rp[i + 1] - rp[i]))
+    sub = spg.CsrMatrix(len(rows), a.ncols, np.array(sub_rp, np.int64), np.concatenate(ci).astype(a.colind.dtype),
+                        np.concatenate(va))
+    da, ds = dev.upload(a), dev.upload(sub)
+    dc = dev.spgemm(ds, da)
+    c = dc.download()
+    dc.free()
+    for t, i in enumerate(rows):
+        e = g["rows"][str(i)]
+        lo, hi = int(c.rowptr[t]), int(c.rowptr[t + 1])
+        cols = np.asarray(c.colind[lo:hi], np.int64)
+        vals = np.asarray(c.values[lo:hi], np.float64)
+        assert hi - lo == e["nnz"], f"row {i} nnz"
+        if "cols" in e:
+            assert cols.tolist() == e["cols"], f"row {i} columns"
+            assert np.array_equal(vals, np.asarray(e["vals"])), f"row {i} values"
+        assert sha(cols) == e["sha_cols"], f"row {i} columns"
+        assert sha(vals) == e["sha_vals"], f"row {i} values"
