@@ -84,9 +84,19 @@ struct RoundPlan {
 struct Pull {
     int round = 0, operand = 0, owner = -1, kslice = -1;  // operand 0 A, 1 B
     int64_t rows = 0, nnz = 0, dev_bytes = 0;
+    bool copied = false;
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     double s0 = 0.0, s1 = 0.0;  // seconds from the rank's start (resolved after the run)
 };
+
+// An in-place read is stamped with the time its rank reached it on the copy
+// stream (after any start delay).
+void stamp(spg_ctx* ctx, cudaStream_t st, Pull& p) {
+    p.t0 = ctx->timer.ev();
+    p.t1 = ctx->timer.ev();
+    SPG_CUDA(cudaEventRecord(p.t0, st));
+    SPG_CUDA(cudaEventRecord(p.t1, st));
+}
 
 struct RankLog {
     std::vector<Pull> pulls;
@@ -111,8 +121,9 @@ __global__ void k_spin_delay(unsigned long long ns) {
 }
 
 // Pulls A tile `av` for round r (copy when it lives elsewhere, in place
-// otherwise) and logs it. SPG_DEBUG_DOUBLE_PULL=1 pulls the first remote A
-// tile twice (fault injection for the ledger tests).
+// otherwise) and logs it. SPG_DEBUG_DOUBLE_PULL=1 (fault injection for the
+// ledger tests) makes the first A tile owned by another rank cost one extra,
+// redundant device copy that is logged like any pull.
 spg_csr* pull_a(spg_ctx* ctx, spg_ctx* cctx, const spg_csr* av, int r, int owner, int rank, bool& owned,
                 RankLog* L, bool& injected) {
     const bool local = av->ctx == ctx && av->storage != 2;
@@ -123,32 +134,37 @@ spg_csr* pull_a(spg_ctx* ctx, spg_ctx* cctx, const spg_csr* av, int r, int owner
     p.owner = owner;
     p.rows = av->nrows;
     p.nnz = av->nnz;
-    if (local) {
-        if (L) L->pulls.push_back(p);
-        return const_cast<spg_csr*>(av);
-    }
-    auto once = [&]() {
+    auto copy = [&]() {
+        Pull q = p;
+        q.copied = true;
         if (L) {
-            p.t0 = ctx->timer.ev();
-            p.t1 = ctx->timer.ev();
-            p.dev_bytes = (av->nrows + 1) * int64_t(sizeof(int64_t)) + av->nnz * int64_t(sizeof(int32_t) + sizeof(double));
-            SPG_CUDA(cudaEventRecord(p.t0, cctx->stream));
+            q.t0 = ctx->timer.ev();
+            q.t1 = ctx->timer.ev();
+            q.dev_bytes = (av->nrows + 1) * int64_t(sizeof(int64_t)) + av->nnz * int64_t(sizeof(int32_t) + sizeof(double));
+            SPG_CUDA(cudaEventRecord(q.t0, cctx->stream));
         }
         spg_csr* c = copy_csr(cctx, av);
         if (L) {
-            SPG_CUDA(cudaEventRecord(p.t1, cctx->stream));
-            L->pulls.push_back(p);
+            SPG_CUDA(cudaEventRecord(q.t1, cctx->stream));
+            L->pulls.push_back(q);
         }
         return c;
     };
     static const char* dbg = std::getenv("SPG_DEBUG_DOUBLE_PULL");
     if (dbg && dbg[0] == '1' && !injected && owner != rank) {
         injected = true;
-        spg_csr* extra = once();
+        spg_csr* extra = copy();
         extra->ctx = cctx;
         free_csr(extra);  // stream-ordered on the copy stream
     }
-    return once();
+    if (local) {
+        if (L) {
+            stamp(ctx, cctx->stream, p);
+            L->pulls.push_back(p);
+        }
+        return const_cast<spg_csr*>(av);
+    }
+    return copy();
 }
 
 void log_b(RankLog* L, const RoundPlan& p, int r, const std::vector<SlicePull>& sl, size_t first) {
@@ -163,6 +179,7 @@ void log_b(RankLog* L, const RoundPlan& p, int r, const std::vector<SlicePull>& 
         u.rows = x.rows;
         u.nnz = x.nnz;
         u.dev_bytes = x.dev_bytes;
+        u.copied = true;
         u.t0 = x.t0;
         u.t1 = x.t1;
         L->pulls.push_back(u);
@@ -311,6 +328,7 @@ spg_csr* run_rank(spg_ctx* ctx, const std::vector<RoundPlan>& plan, const spg_cs
                 u.kslice = p.b_slice[0];
                 u.rows = b0->nrows;
                 u.nnz = b0->nnz;
+                stamp(ctx, cs, u);
                 L->pulls.push_back(u);
             }
         } else {
@@ -463,7 +481,7 @@ void xfer_stats(const std::vector<RankLog>& logs, int rank, double* out) {
     bool any = false;
     for (const Pull& p : logs[rank].pulls) {
         if (p.owner == rank) continue;
-        if (p.dev_bytes == 0 && p.s1 == 0.0) {
+        if (!p.copied) {
             n_inplace += 1;
             continue;
         }
