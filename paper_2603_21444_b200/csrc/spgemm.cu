@@ -46,6 +46,25 @@ __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a,
 
 constexpr unsigned FULL = 0xffffffffu;
 
+// -DSPG_CHECKED: device-side invariant checks (shared-memory indices, bucket
+// ranges, look-back values). A failed check traps, which fails the launch —
+// the checked build is run over the GPU parity tests (compute-sanitizer is
+// not available on the GPU pool).
+#ifdef SPG_CHECKED
+#define SPG_DCHECK(cond)                                                                             \
+    do {                                                                                             \
+        if (!(cond)) {                                                                               \
+            printf("SPG_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+                   blockIdx.x, threadIdx.x);                                                         \
+            __trap();                                                                                \
+        }                                                                                            \
+    } while (0)
+#else
+#define SPG_DCHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 // Monotone map column -> [0, nb): high bits of the column scaled by nb.
 __device__ __forceinline__ int bucket_of(uint32_t col, int cshift, int nb) {
     return static_cast<int>(__umulhi(col << cshift, static_cast<uint32_t>(nb)));
@@ -679,6 +698,7 @@ __device__ __forceinline__ void tile_gather(const TileSmem& S, int ptile, const 
         const int x = threadIdx.x + tile::NT * j;
         if (x < ptile) {
             const int q = S.eof[x];
+            SPG_DCHECK(q >= 0 && q < tile::EMAX);
             const int64_t u = S.ent[q].base + x;
             aux[j] = q;
             col[j] = __ldg(bcol + u);
@@ -707,6 +727,7 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
             val[j] = dadd(0.0, dmul(S.ent[q].av, val[j]));
             const uint32_t bi = S.ebin[q];
             const int b = static_cast<int>(bi & 0xffffu) + bucket_of(col[j], cshift, static_cast<int>(bi >> 16));
+            SPG_DCHECK(b >= 0 && b < 2 * tile::CW * ptile && col[j] >= 0);
             bk[j] = b;
             const int sh = (b & 1) << 4;
             aux[j] = static_cast<int>((atomicAdd(&S.cnt[b >> 1], 1u << sh) >> sh) & 0xffffu);
@@ -754,6 +775,7 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
             const int st = static_cast<int>(r & 0xffffu), sz = static_cast<int>(r >> 16) - st;
             const int slot = aux[j];
             const int pos = st + slot;
+            SPG_DCHECK(pos >= 0 && pos < ptile && sz >= 1 && slot < sz);
             S.col[pos] = col[j];
             if (sz == 1) {
                 S.val[pos] = val[j];
@@ -774,6 +796,7 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
             int b0 = 0;
             if (lane == 0) b0 = atomicAdd(&S.nlist, __popc(has));
             b0 = __shfl_sync(0xffffffffu, b0, 0);
+            SPG_DCHECK(!lreg || b0 + __popc(has & ((1u << lane) - 1u)) < tile::LMAX);
             if (lreg) S.list[b0 + __popc(has & ((1u << lane) - 1u))] = lreg;
         }
     }
@@ -790,6 +813,7 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
         if ((pair >> j) & 1u) {
             const int pos = aux[j] & 0xffff, slot = aux[j] >> 16;
             const int other = pos + 1 - 2 * slot;
+            SPG_DCHECK(other >= 0 && other < ptile);
             const int32_t oc = S.col[other];
             const int ox = S.xs[other];
             const int x = tid + NT * j;
@@ -805,6 +829,7 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
     const int nlist = S.nlist;
     for (int l = tid; l < nlist; l += NT) {
         const int lo = static_cast<int>(S.list[l] & 0xffffu), hi = static_cast<int>(S.list[l] >> 16);
+        SPG_DCHECK(lo >= 0 && lo + 3 <= hi && hi <= ptile);
         for (int a = lo + 1; a < hi; ++a) {
             const int32_t ca = S.col[a];
             const uint16_t xa = S.xs[a];
@@ -866,6 +891,7 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
             double v = S.val[x];
             for (int u = x + 1; u < ptile && ((S.dbm[u >> 5] >> (u & 31)) & 1u); ++u) v = dadd(v, S.val[u]);
             aux[j] = x - dups_before(S, x);
+            SPG_DCHECK(aux[j] >= 0 && aux[j] <= x);
             col[j] = S.col[x];
             val[j] = v;
         }

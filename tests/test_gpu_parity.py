@@ -285,3 +285,27 @@ def test_spgemm_host_entry(dev, shared):
                                   bva.ctypes.data, 4, C.byref(h)))
     c = spg.DeviceCsr(dev, h.value).download()
     assert same(c, O.port_spgemm(a, b))
+
+
+@pytest.mark.parametrize("which", ["er", "rmat", "dups"])
+def test_repeated_multiplies_are_identical(dev, which):
+    """Race stress (compute-sanitizer is not available on the GPU pool): the
+    tile kernel's look-back, relaxed status words and barrier-free pair
+    ranking must give the same bytes on every run, equal to the oracle's."""
+    if which == "er":
+        a = b = spg.gen_erdos_renyi(16384, 8.0 / 16384, 1)
+    elif which == "rmat":
+        a = b = spg.gen_rmat(11, 16, 1, 2)
+    else:  # 3000 x 40 times 40 x 40: nearly every product is a duplicate
+        if not O.ref_available():
+            pytest.skip("needs oracle/_ref for from_triplets")
+        g = O.port_gen_erdos_renyi(3000, 0.01, 3)
+        rows = np.repeat(np.arange(g.nrows), np.diff(np.asarray(g.rowptr)))
+        a = O.ref_from_triplets(g.nrows, 40, rows, np.asarray(g.colind) % 40, np.asarray(g.values))
+        b = O.port_gen_erdos_renyi(40, 0.5, 4)
+    ref = O.port_spgemm(a, b)
+    da = dev.upload(a)
+    db = da if b is a else dev.upload(b)
+    for _ in range(12):
+        c = dev.spgemm(da, db).download()
+        assert same(c, ref)
