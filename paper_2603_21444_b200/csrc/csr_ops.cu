@@ -12,6 +12,7 @@
 
 #include <climits>
 
+#include "block_scan.cuh"
 #include "spg_internal.cuh"
 
 namespace spgb {
@@ -244,37 +245,76 @@ __global__ void k_extract_copy(const int64_t* __restrict__ beg, const int64_t* _
 // stably radix-sorted by column (value as payload), then each column is summed
 // sequentially in storage order, so sums are bit-identical.
 
-// Block per chunk of CS sorted entries, staged in smem with coalesced loads;
-// each run (column) whose head lies in the chunk is summed sequentially in
-// storage order by one thread (reading on into global memory when the run
-// crosses the chunk end). Run ends are found first so the dependent adds can
-// run over an unrolled, known-length loop.
-constexpr int CS_CHUNK = 2048;
-__global__ void __launch_bounds__(256) k_colsum_runs(const int32_t* __restrict__ keys, const double* __restrict__ sval,
-                                                     int64_t nnz, double* __restrict__ colsum) {
-    __shared__ int32_t sk[CS_CHUNK + 1];
-    __shared__ double sv[CS_CHUNK];
-    for (int64_t b = int64_t(blockIdx.x) * CS_CHUNK; b < nnz; b += int64_t(gridDim.x) * CS_CHUNK) {
-        const int n = static_cast<int>(nnz - b < CS_CHUNK ? nnz - b : CS_CHUNK);
-        for (int t = threadIdx.x; t < n; t += blockDim.x) {
-            sk[t + 1] = keys[b + t];
-            sv[t] = sval[b + t];
+// Runs of the sorted keys (one run per column present), in two passes over
+// blocks of CS_BLK keys (16 per thread, 16-byte loads): k_colsum_heads<false>
+// counts each block's run heads, a scan gives each block its first slot,
+// k_colsum_heads<true> writes the head positions in order (heads[nh] = nnz).
+// k_colsum_fold then gives every run one thread that folds its values in
+// storage order: the run [heads[h], heads[h+1]) is contiguous, so its loads
+// are independent (unrolled 8 deep) while the dependent adds retire in order —
+// bit-identical to the reference's loop.
+constexpr int CS_IT = 16, CS_BLK = 256 * CS_IT;
+template <bool WRITE>
+__global__ void __launch_bounds__(256) k_colsum_heads(const int32_t* __restrict__ keys, int64_t nnz,
+                                                      int64_t* __restrict__ bcount, int64_t* __restrict__ heads) {
+    __shared__ int ws[9];
+    const int64_t nblk = (nnz + CS_BLK - 1) / CS_BLK;
+    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const int64_t i0 = blk * CS_BLK + int64_t(threadIdx.x) * CS_IT;
+        int32_t k[CS_IT];
+        uint32_t hm = 0;
+        if (i0 < nnz) {
+            if (i0 + CS_IT <= nnz) {
+#pragma unroll
+                for (int u = 0; u < CS_IT / 4; ++u) {
+                    const int4 w = __ldg(reinterpret_cast<const int4*>(keys + i0) + u);
+                    k[4 * u] = w.x;
+                    k[4 * u + 1] = w.y;
+                    k[4 * u + 2] = w.z;
+                    k[4 * u + 3] = w.w;
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < CS_IT; ++u) k[u] = i0 + u < nnz ? keys[i0 + u] : -1;
+            }
+            int32_t prev = i0 > 0 ? keys[i0 - 1] : -1;
+#pragma unroll
+            for (int u = 0; u < CS_IT; ++u) {
+                if (i0 + u < nnz && k[u] != prev) hm |= 1u << u;
+                prev = k[u];
+            }
         }
-        if (threadIdx.x == 0) sk[0] = b > 0 ? keys[b - 1] : -1;
-        __syncthreads();
-        for (int t = threadIdx.x; t < n; t += blockDim.x) {
-            const int32_t c = sk[t + 1];
-            if (sk[t] == c) continue;  // not a run head
-            int e = t + 1;
-            while (e < n && sk[e + 1] == c) ++e;
-            double acc = 0.0;
-#pragma unroll 8
-            for (int u = t; u < e; ++u) acc = __dadd_rn(acc, sv[u]);
-            if (e == n)  // the run goes on past the chunk
-                for (int64_t u = b + n; u < nnz && keys[u] == c; ++u) acc = __dadd_rn(acc, sval[u]);
-            colsum[c] = acc;
+        int total;
+        const int pre = block_exclusive_scan<256>(__popc(hm), &total, ws);
+        if (!WRITE) {
+            if (threadIdx.x == 0) bcount[blk] = total;
+        } else {
+            int64_t o = bcount[blk] + pre;
+            while (hm) {
+                const int u = __ffs(hm) - 1;
+                hm &= hm - 1;
+                heads[o++] = i0 + u;
+            }
         }
-        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(256) k_colsum_fold(const int32_t* __restrict__ keys, const double* __restrict__ sval,
+                                                     const int64_t* __restrict__ heads, int64_t nh,
+                                                     double* __restrict__ colsum) {
+    for (int64_t h = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; h < nh; h += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t s = heads[h], e = heads[h + 1];
+        double acc = 0.0;
+        int64_t u = s;
+        for (; u + 8 <= e; u += 8) {
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = __ldg(sval + u + q);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc = __dadd_rn(acc, v[q]);
+        }
+        for (; u < e; ++u) acc = __dadd_rn(acc, __ldg(sval + u));
+        colsum[keys[s]] = acc;
     }
 }
 
@@ -766,8 +806,17 @@ void column_sums(spg_ctx* ctx, const spg_csr* m, double* colsum) {
                                                  static_cast<int>(nnz), 0, bits, ctx->stream));
     }
     KTime kt(ctx, "colsum_runs");
-    k_colsum_runs<<<static_cast<int>(std::min<int64_t>((nnz + CS_CHUNK - 1) / CS_CHUNK, int64_t(ctx->num_sms) * 8)), 256,
-                    0, ctx->stream>>>(keys, vals, nnz, colsum);
+    const int64_t nblk = (nnz + CS_BLK - 1) / CS_BLK;
+    const int hg = static_cast<int>(std::min<int64_t>(nblk, int64_t(ctx->num_sms) * 8));
+    DBuf<int64_t> bcount(ctx, nblk), bbase(ctx, nblk + 1), heads(ctx, std::min<int64_t>(nnz, m->ncols) + 1);
+    k_colsum_heads<false><<<hg, 256, 0, ctx->stream>>>(keys, nnz, bcount, nullptr);
+    SPG_LAUNCH_CHECK();
+    exclusive_scan_i64(ctx, bcount, bbase, nblk);
+    k_colsum_heads<true><<<hg, 256, 0, ctx->stream>>>(keys, nnz, bbase, heads);
+    SPG_LAUNCH_CHECK();
+    const int64_t nh = read_scalar(ctx, bbase.get() + nblk);
+    SPG_CUDA(cudaMemcpyAsync(heads.get() + nh, &nnz, sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+    k_colsum_fold<<<grid_for(ctx, nh), 256, 0, ctx->stream>>>(keys, vals, heads, nh, colsum);
     SPG_LAUNCH_CHECK();
 }
 
