@@ -417,17 +417,13 @@ __global__ void __launch_bounds__(256) k_run_count(const K* __restrict__ keys, i
     }
 }
 
-// Each head sums its run sequentially from memory (runs are short except
-// for hub columns, where one thread walks the run and the others skip), and
-// records where its row's output starts (first run of the row) and ends (last
-// run): rows of the batch without products keep start = end = 0.
+// Run heads in order: k_run_heads writes the position of every run head at
+// its output slot (hpos[total] = n is set by the host), so run o is
+// [hpos[o], hpos[o+1]).
 template <typename K>
-__global__ void __launch_bounds__(256) k_run_sum(const K* __restrict__ keys, const double* __restrict__ vals, int64_t n,
-                                                 const int64_t* __restrict__ cbase, int colbits,
-                                                 int32_t* __restrict__ ocol, double* __restrict__ oval,
-                                                 int64_t* __restrict__ rowstart, int64_t* __restrict__ rowend) {
+__global__ void __launch_bounds__(256) k_run_heads(const K* __restrict__ keys, int64_t n,
+                                                   const int64_t* __restrict__ cbase, int64_t* __restrict__ hpos) {
     __shared__ int ws[9];
-    const K cmask = (K(1) << colbits) - 1;
     const int64_t nch = (n + RUN_CH - 1) / RUN_CH;
     for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
         const int64_t i0 = ch * RUN_CH + int64_t(threadIdx.x) * RUN_IT;
@@ -438,17 +434,41 @@ __global__ void __launch_bounds__(256) k_run_sum(const K* __restrict__ keys, con
         while (hm) {
             const int u = __ffs(hm) - 1;
             hm &= hm - 1;
-            const int64_t i = i0 + u;
-            const K key = keys[i];
-            double sum = dadd(0.0, vals[i]);
-            int64_t v = i + 1;
-            for (; v < n && keys[v] == key; ++v) sum = dadd(sum, vals[v]);
-            ocol[o] = static_cast<int32_t>(key & cmask);
-            oval[o] = sum;
-            if (i == 0 || (keys[i - 1] >> colbits) != (key >> colbits)) rowstart[key >> colbits] = o;
-            if (v == n || (keys[v] >> colbits) != (key >> colbits)) rowend[key >> colbits] = o + 1;
-            ++o;
+            hpos[o++] = i0 + u;
         }
+    }
+}
+
+// One thread per run folds its values in sorted order (stable sort: product
+// order = ascending k, so the sum is bit-identical to the reference's
+// acc[j] += av*bv); the run is contiguous, so its loads are independent and
+// unrolled 8 deep (hub columns make runs of thousands). The first and last
+// run of a row record where the row's output starts and ends (rows of the
+// batch without products keep start = end = 0).
+template <typename K>
+__global__ void __launch_bounds__(256) k_run_fold(const K* __restrict__ keys, const double* __restrict__ vals,
+                                                  const int64_t* __restrict__ hpos, int64_t total, int colbits,
+                                                  int32_t* __restrict__ ocol, double* __restrict__ oval,
+                                                  int64_t* __restrict__ rowstart, int64_t* __restrict__ rowend) {
+    const K cmask = (K(1) << colbits) - 1;
+    for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < total; o += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t s = hpos[o], e = hpos[o + 1];
+        const K key = keys[s];
+        double sum = dadd(0.0, vals[s]);
+        int64_t u = s + 1;
+        for (; u + 8 <= e; u += 8) {
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = __ldg(vals + u + q);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sum = dadd(sum, v[q]);
+        }
+        for (; u < e; ++u) sum = dadd(sum, __ldg(vals + u));
+        ocol[o] = static_cast<int32_t>(key & cmask);
+        oval[o] = sum;
+        const K row = key >> colbits;
+        if (o == 0 || (keys[hpos[o - 1]] >> colbits) != row) rowstart[row] = o;
+        if (o + 1 == total || (keys[e] >> colbits) != row) rowend[row] = o + 1;
     }
 }
 
@@ -1235,12 +1255,20 @@ int64_t big_rows_esc(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const int
         SPG_CUDA(cudaMemsetAsync(rend.get(), 0, (nb + 1) * sizeof(int64_t), ctx->stream));
         {
             KTime kr(ctx, "big_runs");
-            if (k32)
-                k_run_sum<uint32_t><<<rgrid, 256, 0, ctx->stream>>>((uint32_t*)keys2.get(), vals2, P, cbase, colbits,
-                                                                    outc.back()->get(), outv.back()->get(), rstart, rend);
-            else
-                k_run_sum<uint64_t><<<rgrid, 256, 0, ctx->stream>>>((uint64_t*)keys2.get(), vals2, P, cbase, colbits,
-                                                                    outc.back()->get(), outv.back()->get(), rstart, rend);
+            DBuf<int64_t> hpos(ctx, total + 1);
+            SPG_CUDA(cudaMemcpyAsync(hpos.get() + total, &P, sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+            const int fg = grid_for(ctx, total);
+            if (k32) {
+                k_run_heads<uint32_t><<<rgrid, 256, 0, ctx->stream>>>((uint32_t*)keys2.get(), P, cbase, hpos);
+                SPG_LAUNCH_CHECK();
+                k_run_fold<uint32_t><<<fg, 256, 0, ctx->stream>>>((uint32_t*)keys2.get(), vals2, hpos, total, colbits,
+                                                                  outc.back()->get(), outv.back()->get(), rstart, rend);
+            } else {
+                k_run_heads<uint64_t><<<rgrid, 256, 0, ctx->stream>>>((uint64_t*)keys2.get(), P, cbase, hpos);
+                SPG_LAUNCH_CHECK();
+                k_run_fold<uint64_t><<<fg, 256, 0, ctx->stream>>>((uint64_t*)keys2.get(), vals2, hpos, total, colbits,
+                                                                  outc.back()->get(), outv.back()->get(), rstart, rend);
+            }
             SPG_LAUNCH_CHECK();
         }
         k_big_finish<<<grid_for(ctx, nb), 256, 0, ctx->stream>>>(drows + r0, nb, rstart, rend, outc.back()->get(),
