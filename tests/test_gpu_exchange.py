@@ -113,10 +113,14 @@ def test_node_start_delay_on_the_device():
     assert np.array_equal(r.ledger, ref["ledger"])
     assert ours_multiset(r) == ref_multiset("trident", a, b, 8, 2, delays)
     pulls = [e for e in r.events if e["type"] == "transfer-complete"]
-    late = [e["t_start"] for e in pulls if e["dst"] // 2 == 1]
-    early = [e["t_start"] for e in pulls if e["dst"] // 2 == 0]
-    assert late and min(late) >= 0.05
-    assert early and max(early) < 0.05
+    first = {}
+    for e in pulls:
+        first[e["dst"]] = min(first.get(e["dst"], 1e9), e["t_start"])
+    # every rank of node 1 starts pulling after its 50 ms delay; node 0's ranks
+    # start at once (later pulls of theirs may queue behind a delayed owner's
+    # copies on a multi-GPU box, so only the first pull is compared)
+    assert all(first[r] >= 0.05 for r in (2, 3))
+    assert all(first[r] < 0.05 for r in (0, 1))
     with pytest.raises(spg.SpgError):
         spg.trident_spgemm(a, b, grid, node_start_delay=[-1.0])
 
