@@ -550,6 +550,7 @@ def ours_multi(args):
             "kernel_ms_rank0": {k: round(v[1] / max(1, v[0]), 4) for k, v in kt.items()},
             "exchange": {"ledger_max_recv_bytes_per_rank": recv_bytes, "exchange_ms_rank0": round(exch_ms, 4),
                          "nvlink_frac_rank0": round(recv_bytes / max(exch_ms, 1e-9) / 1e6 / NVLINK_GBS, 4),
+                         "nvlink_frac_rank0_of_measured_peer_copy": round(recv_bytes / max(exch_ms, 1e-9) / 1e6 / 770.0, 4),
                          "nvlink_peak_gbs": NVLINK_GBS},
             "roofline": roof0,
             "e2e": {"value": round(2.0 * products_total / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",

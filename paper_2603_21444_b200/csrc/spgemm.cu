@@ -487,6 +487,150 @@ __global__ void k_big_finish(const int32_t* __restrict__ rows, int nrows, const 
     }
 }
 
+// ------------------------------------------- BIG rows: dense hub accumulator
+// Rows too large for a tile (R-MAT hubs: up to 3.6e7 products) without a
+// sort. One CTA per row (rows from a ticket). The columns are processed in
+// windows of HUB_W = HUB_NW * HUB_RANGE; in a window, warp w owns the column
+// range [base + w*HUB_RANGE, base + (w+1)*HUB_RANGE): a shared-memory bitmap
+// of the columns it has touched and, for the numeric pass, their running sums
+// in a per-CTA scratch (HUB_W doubles). Every warp walks the row's entries in
+// ascending k: 32 lanes binary-search 32 entries' B rows for the warp's column
+// range at once, then the entries are applied one after another (__syncwarp
+// between them) with the lanes over the entry's columns in that range — the
+// columns of one B row are distinct, so no two lanes touch the same column, and
+// every column's sum is 0 + a*b, then + a*b in ascending k: bit-identical to
+// the reference's acc[j] += av*bv. The symbolic pass only counts the distinct
+// columns (side_nnz, what k_tile needs for the row pointers); the numeric pass
+// runs after k_tile and writes each warp's columns in order straight into C
+// at the row's offset.
+constexpr int HUB_NW = 8, HUB_RANGE = 32768, HUB_W = HUB_NW * HUB_RANGE, HUB_WORDS = HUB_RANGE / 32;
+
+// First position in bcol[lo, hi) with column >= c (the B row is sorted).
+__device__ __forceinline__ int64_t lower_col(const int32_t* __restrict__ bcol, int64_t lo, int64_t hi, int64_t c) {
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(bcol + mid) < c) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+template <bool NUMERIC>
+__global__ void __launch_bounds__(32 * HUB_NW) k_hub(const int32_t* __restrict__ rows, int nrows,
+                                                     const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
+                                                     const double* __restrict__ aval, const int64_t* __restrict__ brp,
+                                                     const int32_t* __restrict__ bcol, const double* __restrict__ bval,
+                                                     int64_t ncols, unsigned* __restrict__ ticket,
+                                                     double* __restrict__ scratch, int64_t* __restrict__ side_nnz,
+                                                     const int64_t* __restrict__ crp, int32_t* __restrict__ ccol,
+                                                     double* __restrict__ cval) {
+    __shared__ uint32_t bm[HUB_NW][HUB_WORDS];
+    __shared__ int s_row;
+    __shared__ int64_t s_cnt[HUB_NW];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t* my = bm[warp];
+    double* acc = scratch + static_cast<size_t>(blockIdx.x) * HUB_W + static_cast<size_t>(warp) * HUB_RANGE;
+    while (true) {
+        if (threadIdx.x == 0) s_row = static_cast<int>(atomicAdd(ticket, 1u));
+        __syncthreads();
+        const int t = s_row;
+        __syncthreads();
+        if (t >= nrows) break;
+        const int64_t i = rows[t];
+        const int64_t e0 = arp[i], e1 = arp[i + 1];
+        int64_t done = 0;  // C entries of the row written / counted so far (earlier windows)
+        for (int64_t wbase = 0; wbase < ncols; wbase += HUB_W) {
+            const int64_t lo_c = wbase + int64_t(warp) * HUB_RANGE, hi_c = lo_c + HUB_RANGE;
+            for (int x = lane; x < HUB_WORDS; x += 32) my[x] = 0u;
+            __syncwarp();
+            if (lo_c < ncols) {
+                for (int64_t c0 = e0; c0 < e1; c0 += 32) {
+                    // lane q: the part of entry c0 + q's B row inside [lo_c, hi_c)
+                    const int64_t e = c0 + lane;
+                    int64_t s = 0, f = 0;
+                    double av = 0.0;
+                    if (e < e1) {
+                        const int32_t k = __ldg(acol + e);
+                        const int64_t bs = __ldg(brp + k), be = __ldg(brp + k + 1);
+                        if (bs < be && __ldg(bcol + bs) < hi_c && __ldg(bcol + be - 1) >= lo_c) {
+                            s = lower_col(bcol, bs, be, lo_c);
+                            f = lower_col(bcol, s, be, hi_c);
+                        }
+                        if (NUMERIC) av = __ldg(aval + e);
+                    }
+                    const int ne = static_cast<int>(min(int64_t(32), e1 - c0));
+                    for (int q = 0; q < ne; ++q) {  // the entries in ascending k
+                        const int64_t qs = __shfl_sync(FULL, s, q), qf = __shfl_sync(FULL, f, q);
+                        const double qa = NUMERIC ? __shfl_sync(FULL, av, q) : 0.0;
+                        // 4 elements per lane in flight: the columns of one
+                        // B row are distinct, so their sums never alias
+                        for (int64_t u0 = qs + lane; u0 < qf; u0 += 128) {
+                            int b[4];
+                            double p[4], a4[4];
+                            uint32_t first = 0;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const int64_t u = u0 + 32 * j;
+                                b[j] = u < qf ? static_cast<int>(__ldg(bcol + u) - lo_c) : -1;
+                                if (NUMERIC) p[j] = u < qf ? dmul(qa, __ldg(bval + u)) : 0.0;
+                            }
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                if (b[j] >= 0) {
+                                    const uint32_t bit = 1u << (b[j] & 31);
+                                    if (!(atomicOr(&my[b[j] >> 5], bit) & bit)) first |= 1u << j;
+                                }
+                            if (NUMERIC) {
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) a4[j] = (b[j] >= 0 && !((first >> j) & 1)) ? acc[b[j]] : 0.0;
+#pragma unroll
+                                for (int j = 0; j < 4; ++j)
+                                    if (b[j] >= 0) acc[b[j]] = ((first >> j) & 1) ? dadd(0.0, p[j]) : dadd(a4[j], p[j]);
+                            }
+                        }
+                        __syncwarp();
+                    }
+                }
+            }
+            // the warp's distinct columns of this window
+            int64_t cnt = 0;
+            for (int x = lane; x < HUB_WORDS; x += 32) cnt += __popc(my[x]);
+            cnt = warp_reduce_sum(cnt);
+            if (lane == 0) s_cnt[warp] = cnt;
+            __syncthreads();
+            int64_t before = 0, total = 0;
+#pragma unroll
+            for (int w = 0; w < HUB_NW; ++w) {
+                before += w < warp ? s_cnt[w] : 0;
+                total += s_cnt[w];
+            }
+            if (NUMERIC) {
+                // the warp's columns in order: words in order, bits in order
+                int64_t o = crp[i] + done + before;
+                for (int x0 = 0; x0 < HUB_WORDS; x0 += 32) {
+                    const uint32_t wd = my[x0 + lane];
+                    const int c = __popc(wd);
+                    const int inc = warp_inclusive_scan(c);
+                    int64_t p = o + inc - c;
+                    uint32_t r = wd;
+                    while (r) {
+                        const int bpos = __ffs(r) - 1;
+                        r &= r - 1;
+                        const int b = (x0 + lane) * 32 + bpos;
+                        ccol[p] = static_cast<int32_t>(lo_c + b);
+                        cval[p] = acc[b];
+                        ++p;
+                    }
+                    o += __shfl_sync(FULL, inc, 31);
+                }
+            }
+            done += total;
+            __syncthreads();
+        }
+        if (!NUMERIC && threadIdx.x == 0) side_nnz[i] = done;
+    }
+}
+
 // BIG rows' sorted products into C[crp[r], crp[r+1]) (after k_rows wrote the
 // row pointers): one CTA-range per row chunk, 16 independent copies per thread
 // in flight.
@@ -1121,7 +1265,80 @@ struct HostProf {
     }
 };
 
-// BIG rows: sort-based ESC in memory-bounded batches of consecutive big rows.
+// BIG rows, dense hub path (k_hub) when the columns fit one window: the
+// symbolic pass sizes the rows (side_nnz) for k_tile; the numeric pass runs
+// after k_tile (hub_numeric). drows receives the BIG rows in ascending order.
+constexpr int64_t HUB_MAX_COLS = HUB_W;
+int hub_grid(spg_ctx* ctx) {
+    static const char* g = std::getenv("SPG_HUB_CTAS");
+    return ctx->num_sms * (g ? std::atoi(g) : 2);
+}
+
+int64_t hub_symbolic(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const int32_t* big_list, int nbig,
+                     const int64_t* prod, int32_t* drows, int64_t* side_nnz, int64_t* big_products) {
+    // the rows, heaviest first (each row is one CTA's job: the long ones
+    // must not start last)
+    std::vector<int32_t> hrows(nbig);
+    SPG_CUDA(cudaMemcpyAsync(hrows.data(), big_list, nbig * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::sort(hrows.begin(), hrows.end());
+    DBuf<int64_t> dprod(ctx, nbig), dnnz(ctx, nbig), sums(ctx, 2);
+    {
+        SPG_CUDA(cudaMemcpyAsync(drows, hrows.data(), nbig * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+        k_side_gather<<<grid_for(ctx, nbig), 256, 0, ctx->stream>>>(drows, nbig, prod, dprod);
+        SPG_LAUNCH_CHECK();
+        std::vector<int64_t> hp(nbig);
+        SPG_CUDA(cudaMemcpyAsync(hp.data(), dprod.get(), nbig * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+        std::vector<int> ord(nbig);
+        for (int r = 0; r < nbig; ++r) ord[r] = r;
+        std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return hp[x] > hp[y]; });
+        std::vector<int32_t> sorted(nbig);
+        for (int r = 0; r < nbig; ++r) sorted[r] = hrows[ord[r]];
+        hrows.swap(sorted);
+        SPG_CUDA(cudaMemcpyAsync(drows, hrows.data(), nbig * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+        SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    DBuf<unsigned> ticket(ctx, 1);
+    SPG_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), ctx->stream));
+    {
+        KTime kt(ctx, "hub_symbolic");
+        k_hub<false><<<hub_grid(ctx), 32 * HUB_NW, 0, ctx->stream>>>(drows, nbig, a->rowptr, a->colind, a->values,
+                                                                    b->rowptr, b->colind, b->values, b->ncols,
+                                                                    ticket, nullptr, side_nnz, nullptr, nullptr,
+                                                                    nullptr);
+        SPG_LAUNCH_CHECK();
+    }
+    k_side_gather<<<grid_for(ctx, nbig), 256, 0, ctx->stream>>>(drows, nbig, prod, dprod);
+    SPG_LAUNCH_CHECK();
+    k_side_gather<<<grid_for(ctx, nbig), 256, 0, ctx->stream>>>(drows, nbig, side_nnz, dnnz);
+    SPG_LAUNCH_CHECK();
+    size_t tmp = 0;
+    SPG_CUDA(cub::DeviceReduce::Sum(nullptr, tmp, dprod.get(), sums.get(), nbig, ctx->stream));
+    DBuf<unsigned char> t(ctx, tmp);
+    SPG_CUDA(cub::DeviceReduce::Sum(t.get(), tmp, dprod.get(), sums.get(), nbig, ctx->stream));
+    SPG_CUDA(cub::DeviceReduce::Sum(t.get(), tmp, dnnz.get(), sums.get() + 1, nbig, ctx->stream));
+    int64_t h[2];
+    SPG_CUDA(cudaMemcpyAsync(h, sums.get(), sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+    *big_products = h[0];
+    return h[1];
+}
+
+void hub_numeric(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const int32_t* drows, int nbig, spg_csr* c) {
+    const int grid = hub_grid(ctx);
+    DBuf<double> scratch(ctx, static_cast<size_t>(grid) * HUB_W);
+    DBuf<unsigned> ticket(ctx, 1);
+    SPG_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), ctx->stream));
+    KTime kt(ctx, "hub_numeric");
+    k_hub<true><<<grid, 32 * HUB_NW, 0, ctx->stream>>>(drows, nbig, a->rowptr, a->colind, a->values, b->rowptr,
+                                                        b->colind, b->values, b->ncols, ticket, scratch, nullptr,
+                                                        c->rowptr, c->colind, c->values);
+    SPG_LAUNCH_CHECK();
+}
+
+// BIG rows: sort-based ESC in memory-bounded batches of consecutive big rows
+// (matrices wider than one hub window).
 // Fills side_cp/side_vp/side_nnz (per row of A) and keeps the batch outputs
 // alive in outc/outv until k_big_copy has moved them into C.
 int64_t big_rows_esc(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const int32_t* big_list, int nbig,
@@ -1337,10 +1554,15 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEven
     std::vector<std::unique_ptr<DBuf<int32_t>>> outc;
     std::vector<std::unique_ptr<DBuf<double>>> outv;
     int64_t big_products = 0, big_nnz = 0;  // C capacity = products of tile rows + exact nnz of big rows
+    static const char* esc_env = std::getenv("SPG_BIG_ESC");
+    const bool hub = b->ncols <= HUB_MAX_COLS && !(esc_env && esc_env[0] == '1');
     if (nbig) {
         KTime kt(ctx, "big_rows");
-        big_nnz = big_rows_esc(ctx, a, b, big_list, nbig, prod, drows, side_cp, side_vp, side_nnz, outc, outv, hprof,
-                               &big_products);
+        if (hub)
+            big_nnz = hub_symbolic(ctx, a, b, big_list, nbig, prod, drows, side_nnz, &big_products);
+        else
+            big_nnz = big_rows_esc(ctx, a, b, big_list, nbig, prod, drows, side_cp, side_vp, side_nnz, outc, outv,
+                                   hprof, &big_products);
     }
     hprof.mark("side");
     // 4: tiles
@@ -1371,7 +1593,9 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEven
                                                                   side_nnz, status, c->rowptr, c->colind, c->values);
         SPG_LAUNCH_CHECK();
     }
-    if (nbig) {
+    if (nbig && hub) {
+        hub_numeric(ctx, a, b, drows, nbig, c);
+    } else if (nbig) {
         KTime kt(ctx, "big_copy");
         k_big_copy<<<std::min(nbig, ctx->num_sms * 8), 256, 0, ctx->stream>>>(drows, nbig, side_cp, side_vp,
                                                                              c->rowptr, c->colind, c->values);
