@@ -489,21 +489,30 @@ __global__ void k_big_finish(const int32_t* __restrict__ rows, int nrows, const 
 
 // ------------------------------------------- BIG rows: dense hub accumulator
 // Rows too large for a tile (R-MAT hubs: up to 3.6e7 products) without a
-// sort. One CTA per row (rows from a ticket). The columns are processed in
-// windows of HUB_W = HUB_NW * HUB_RANGE; in a window, warp w owns the column
-// range [base + w*HUB_RANGE, base + (w+1)*HUB_RANGE): a shared-memory bitmap
-// of the columns it has touched and, for the numeric pass, their running sums
-// in a per-CTA scratch (HUB_W doubles). Every warp walks the row's entries in
-// ascending k: 32 lanes binary-search 32 entries' B rows for the warp's column
-// range at once, then the entries are applied one after another (__syncwarp
-// between them) with the lanes over the entry's columns in that range — the
-// columns of one B row are distinct, so no two lanes touch the same column, and
-// every column's sum is 0 + a*b, then + a*b in ascending k: bit-identical to
-// the reference's acc[j] += av*bv. The symbolic pass only counts the distinct
-// columns (side_nnz, what k_tile needs for the row pointers); the numeric pass
-// runs after k_tile and writes each warp's columns in order straight into C
-// at the row's offset.
+// sort, for B with at most HUB_W columns. One CTA per row (rows from a
+// ticket, heaviest first); warp w owns the column range [w*HUB_RANGE,
+// (w+1)*HUB_RANGE) with a shared-memory bitmap of its columns.
+//  * symbolic (k_hub_sym): every warp walks the row's entries — 32 lanes
+//    binary-search 32 entries' B rows for the warp's range at once, then set
+//    the bits of the entries' columns — and stores its bitmap; the row's nnz
+//    (side_nnz) sizes k_tile's row pointers.
+//  * numeric (k_hub_num, after k_tile): the warp loads its bitmap and the
+//    prefix of its words' popcounts, so column c of the row is C entry
+//    crp[i] + (earlier warps' columns) + rank(c). The entries are applied in
+//    ascending k, one after another (__syncwarp between them), the lanes over
+//    the entry's columns in the range — distinct, so no two lanes share an
+//    entry of C — and every C entry is 0 + a*b (first touch, a second bitmap),
+//    then + a*b in ascending k, accumulated in place in C: bit-identical to the
+//    reference's acc[j] += av*bv. The running sums live in the row's own C
+//    range (compact, L2-resident), not in a dense scratch.
 constexpr int HUB_NW = 8, HUB_RANGE = 32768, HUB_W = HUB_NW * HUB_RANGE, HUB_WORDS = HUB_RANGE / 32;
+struct HubSmem {
+    uint32_t sb[HUB_NW][HUB_WORDS];  // the row's columns (symbolic bitmap)
+    uint32_t sp[HUB_NW][HUB_WORDS];  // exclusive prefix of the words' popcounts
+    uint32_t bm[HUB_NW][HUB_WORDS];  // touched so far (numeric)
+    int64_t cnt[HUB_NW];
+    int row;
+};
 
 // First position in bcol[lo, hi) with column >= c (the B row is sorted).
 __device__ __forceinline__ int64_t lower_col(const int32_t* __restrict__ bcol, int64_t lo, int64_t hi, int64_t c) {
@@ -515,119 +524,174 @@ __device__ __forceinline__ int64_t lower_col(const int32_t* __restrict__ bcol, i
     return lo;
 }
 
-template <bool NUMERIC>
-__global__ void __launch_bounds__(32 * HUB_NW) k_hub(const int32_t* __restrict__ rows, int nrows,
-                                                     const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
-                                                     const double* __restrict__ aval, const int64_t* __restrict__ brp,
-                                                     const int32_t* __restrict__ bcol, const double* __restrict__ bval,
-                                                     int64_t ncols, unsigned* __restrict__ ticket,
-                                                     double* __restrict__ scratch, int64_t* __restrict__ side_nnz,
-                                                     const int64_t* __restrict__ crp, int32_t* __restrict__ ccol,
-                                                     double* __restrict__ cval) {
-    __shared__ uint32_t bm[HUB_NW][HUB_WORDS];
-    __shared__ int s_row;
-    __shared__ int64_t s_cnt[HUB_NW];
+// The part [s, f) of entry e's B row inside [lo_c, hi_c), with its A value.
+__device__ __forceinline__ void hub_span(const int32_t* __restrict__ acol, const double* __restrict__ aval,
+                                         const int64_t* __restrict__ brp, const int32_t* __restrict__ bcol,
+                                         int64_t e, int64_t e1, int64_t lo_c, int64_t hi_c, int64_t& s, int64_t& f,
+                                         double& av, bool want_av) {
+    s = f = 0;
+    av = 0.0;
+    if (e >= e1) return;
+    const int32_t k = __ldg(acol + e);
+    const int64_t bs = __ldg(brp + k), be = __ldg(brp + k + 1);
+    if (bs < be && __ldg(bcol + bs) < hi_c && __ldg(bcol + be - 1) >= lo_c) {
+        s = lower_col(bcol, bs, be, lo_c);
+        f = lower_col(bcol, s, be, hi_c);
+    }
+    if (want_av) av = __ldg(aval + e);
+}
+
+__global__ void __launch_bounds__(32 * HUB_NW) k_hub_sym(const int32_t* __restrict__ rows, int nrows,
+                                                         const int64_t* __restrict__ arp,
+                                                         const int32_t* __restrict__ acol,
+                                                         const int64_t* __restrict__ brp,
+                                                         const int32_t* __restrict__ bcol, unsigned* __restrict__ ticket,
+                                                         uint32_t* __restrict__ gbm, int64_t* __restrict__ side_nnz) {
+    extern __shared__ __align__(16) unsigned char hub_raw[];
+    HubSmem& S = *reinterpret_cast<HubSmem*>(hub_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t* my = bm[warp];
-    double* acc = scratch + static_cast<size_t>(blockIdx.x) * HUB_W + static_cast<size_t>(warp) * HUB_RANGE;
+    uint32_t* my = S.bm[warp];
+    const int64_t lo_c = int64_t(warp) * HUB_RANGE, hi_c = lo_c + HUB_RANGE;
     while (true) {
-        if (threadIdx.x == 0) s_row = static_cast<int>(atomicAdd(ticket, 1u));
+        if (threadIdx.x == 0) S.row = static_cast<int>(atomicAdd(ticket, 1u));
         __syncthreads();
-        const int t = s_row;
+        const int t = S.row;
         __syncthreads();
         if (t >= nrows) break;
         const int64_t i = rows[t];
         const int64_t e0 = arp[i], e1 = arp[i + 1];
-        int64_t done = 0;  // C entries of the row written / counted so far (earlier windows)
-        for (int64_t wbase = 0; wbase < ncols; wbase += HUB_W) {
-            const int64_t lo_c = wbase + int64_t(warp) * HUB_RANGE, hi_c = lo_c + HUB_RANGE;
-            for (int x = lane; x < HUB_WORDS; x += 32) my[x] = 0u;
-            __syncwarp();
-            if (lo_c < ncols) {
-                for (int64_t c0 = e0; c0 < e1; c0 += 32) {
-                    // lane q: the part of entry c0 + q's B row inside [lo_c, hi_c)
-                    const int64_t e = c0 + lane;
-                    int64_t s = 0, f = 0;
-                    double av = 0.0;
-                    if (e < e1) {
-                        const int32_t k = __ldg(acol + e);
-                        const int64_t bs = __ldg(brp + k), be = __ldg(brp + k + 1);
-                        if (bs < be && __ldg(bcol + bs) < hi_c && __ldg(bcol + be - 1) >= lo_c) {
-                            s = lower_col(bcol, bs, be, lo_c);
-                            f = lower_col(bcol, s, be, hi_c);
-                        }
-                        if (NUMERIC) av = __ldg(aval + e);
-                    }
-                    const int ne = static_cast<int>(min(int64_t(32), e1 - c0));
-                    for (int q = 0; q < ne; ++q) {  // the entries in ascending k
-                        const int64_t qs = __shfl_sync(FULL, s, q), qf = __shfl_sync(FULL, f, q);
-                        const double qa = NUMERIC ? __shfl_sync(FULL, av, q) : 0.0;
-                        // 4 elements per lane in flight: the columns of one
-                        // B row are distinct, so their sums never alias
-                        for (int64_t u0 = qs + lane; u0 < qf; u0 += 128) {
-                            int b[4];
-                            double p[4], a4[4];
-                            uint32_t first = 0;
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                const int64_t u = u0 + 32 * j;
-                                b[j] = u < qf ? static_cast<int>(__ldg(bcol + u) - lo_c) : -1;
-                                if (NUMERIC) p[j] = u < qf ? dmul(qa, __ldg(bval + u)) : 0.0;
-                            }
-#pragma unroll
-                            for (int j = 0; j < 4; ++j)
-                                if (b[j] >= 0) {
-                                    const uint32_t bit = 1u << (b[j] & 31);
-                                    if (!(atomicOr(&my[b[j] >> 5], bit) & bit)) first |= 1u << j;
-                                }
-                            if (NUMERIC) {
-#pragma unroll
-                                for (int j = 0; j < 4; ++j) a4[j] = (b[j] >= 0 && !((first >> j) & 1)) ? acc[b[j]] : 0.0;
-#pragma unroll
-                                for (int j = 0; j < 4; ++j)
-                                    if (b[j] >= 0) acc[b[j]] = ((first >> j) & 1) ? dadd(0.0, p[j]) : dadd(a4[j], p[j]);
-                            }
-                        }
-                        __syncwarp();
-                    }
+        for (int x = lane; x < HUB_WORDS; x += 32) my[x] = 0u;
+        __syncwarp();
+        for (int64_t c0 = e0; c0 < e1; c0 += 32) {
+            int64_t s, f;
+            double av;
+            hub_span(acol, nullptr, brp, bcol, c0 + lane, e1, lo_c, hi_c, s, f, av, false);
+            const int ne = static_cast<int>(min(int64_t(32), e1 - c0));
+            for (int q = 0; q < ne; ++q) {  // order does not matter for the count
+                const int64_t qs = __shfl_sync(FULL, s, q), qf = __shfl_sync(FULL, f, q);
+                for (int64_t u = qs + lane; u < qf; u += 32) {
+                    const int b = static_cast<int>(__ldg(bcol + u) - lo_c);
+                    atomicOr(&my[b >> 5], 1u << (b & 31));
                 }
             }
-            // the warp's distinct columns of this window
-            int64_t cnt = 0;
-            for (int x = lane; x < HUB_WORDS; x += 32) cnt += __popc(my[x]);
-            cnt = warp_reduce_sum(cnt);
-            if (lane == 0) s_cnt[warp] = cnt;
-            __syncthreads();
-            int64_t before = 0, total = 0;
-#pragma unroll
-            for (int w = 0; w < HUB_NW; ++w) {
-                before += w < warp ? s_cnt[w] : 0;
-                total += s_cnt[w];
-            }
-            if (NUMERIC) {
-                // the warp's columns in order: words in order, bits in order
-                int64_t o = crp[i] + done + before;
-                for (int x0 = 0; x0 < HUB_WORDS; x0 += 32) {
-                    const uint32_t wd = my[x0 + lane];
-                    const int c = __popc(wd);
-                    const int inc = warp_inclusive_scan(c);
-                    int64_t p = o + inc - c;
-                    uint32_t r = wd;
-                    while (r) {
-                        const int bpos = __ffs(r) - 1;
-                        r &= r - 1;
-                        const int b = (x0 + lane) * 32 + bpos;
-                        ccol[p] = static_cast<int32_t>(lo_c + b);
-                        cval[p] = acc[b];
-                        ++p;
-                    }
-                    o += __shfl_sync(FULL, inc, 31);
-                }
-            }
-            done += total;
-            __syncthreads();
         }
-        if (!NUMERIC && threadIdx.x == 0) side_nnz[i] = done;
+        __syncwarp();
+        int64_t cnt = 0;
+        uint32_t* g = gbm + static_cast<size_t>(t) * (HUB_W / 32) + static_cast<size_t>(warp) * HUB_WORDS;
+        for (int x = lane; x < HUB_WORDS; x += 32) {
+            const uint32_t w = my[x];
+            g[x] = w;
+            cnt += __popc(w);
+        }
+        cnt = warp_reduce_sum(cnt);
+        if (lane == 0) S.cnt[warp] = cnt;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int64_t tot = 0;
+            for (int w = 0; w < HUB_NW; ++w) tot += S.cnt[w];
+            side_nnz[i] = tot;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(32 * HUB_NW) k_hub_num(const int32_t* __restrict__ rows, int nrows,
+                                                         const int64_t* __restrict__ arp,
+                                                         const int32_t* __restrict__ acol,
+                                                         const double* __restrict__ aval,
+                                                         const int64_t* __restrict__ brp,
+                                                         const int32_t* __restrict__ bcol,
+                                                         const double* __restrict__ bval, unsigned* __restrict__ ticket,
+                                                         const uint32_t* __restrict__ gbm,
+                                                         const int64_t* __restrict__ crp, int32_t* __restrict__ ccol,
+                                                         double* __restrict__ cval) {
+    extern __shared__ __align__(16) unsigned char hub_raw[];
+    HubSmem& S = *reinterpret_cast<HubSmem*>(hub_raw);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t* sb = S.sb[warp];
+    uint32_t* sp = S.sp[warp];
+    uint32_t* bm = S.bm[warp];
+    const int64_t lo_c = int64_t(warp) * HUB_RANGE, hi_c = lo_c + HUB_RANGE;
+    constexpr int WPL = HUB_WORDS / 32;  // words per lane (contiguous)
+    while (true) {
+        if (threadIdx.x == 0) S.row = static_cast<int>(atomicAdd(ticket, 1u));
+        __syncthreads();
+        const int t = S.row;
+        __syncthreads();
+        if (t >= nrows) break;
+        const int64_t i = rows[t];
+        const int64_t e0 = arp[i], e1 = arp[i + 1];
+        // this warp's bitmap, the prefix of its popcounts, and its first C entry
+        const uint32_t* g = gbm + static_cast<size_t>(t) * (HUB_W / 32) + static_cast<size_t>(warp) * HUB_WORDS;
+        uint32_t wsum = 0;
+#pragma unroll 8
+        for (int u = 0; u < WPL; ++u) {
+            const uint32_t w = g[lane * WPL + u];
+            sb[lane * WPL + u] = w;
+            bm[lane * WPL + u] = 0u;
+            wsum += __popc(w);
+        }
+        const uint32_t winc = warp_inclusive_scan(wsum);
+        {
+            uint32_t e = winc - wsum;
+            for (int u = 0; u < WPL; ++u) {
+                sp[lane * WPL + u] = e;
+                e += __popc(sb[lane * WPL + u]);
+            }
+        }
+        if (lane == 31) S.cnt[warp] = winc;
+        __syncthreads();
+        int64_t base = crp[i];
+        for (int w = 0; w < warp; ++w) base += S.cnt[w];
+        int32_t* oc = ccol + base;
+        double* ov = cval + base;
+        for (int64_t c0 = e0; c0 < e1; c0 += 32) {
+            int64_t s, f;
+            double av;
+            hub_span(acol, aval, brp, bcol, c0 + lane, e1, lo_c, hi_c, s, f, av, true);
+            const int ne = static_cast<int>(min(int64_t(32), e1 - c0));
+            for (int q = 0; q < ne; ++q) {  // the entries in ascending k
+                const int64_t qs = __shfl_sync(FULL, s, q), qf = __shfl_sync(FULL, f, q);
+                const double qa = __shfl_sync(FULL, av, q);
+                // 4 elements per lane in flight: the columns of one B row are
+                // distinct, so their C entries never alias
+                for (int64_t u0 = qs + lane; u0 < qf; u0 += 128) {
+                    int r[4];
+                    int32_t cc[4];
+                    double p[4], cur[4];
+                    uint32_t first = 0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int64_t u = u0 + 32 * j;
+                        cc[j] = u < qf ? __ldg(bcol + u) : -1;
+                        p[j] = u < qf ? dmul(qa, __ldg(bval + u)) : 0.0;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        r[j] = -1;
+                        if (cc[j] >= 0) {
+                            const int b = static_cast<int>(cc[j] - lo_c), wd = b >> 5;
+                            const uint32_t bit = 1u << (b & 31);
+                            r[j] = static_cast<int>(sp[wd] + __popc(sb[wd] & (bit - 1u)));
+                            if (!(atomicOr(&bm[wd], bit) & bit)) first |= 1u << j;
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) cur[j] = (r[j] >= 0 && !((first >> j) & 1)) ? ov[r[j]] : 0.0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (r[j] >= 0) {
+                            if ((first >> j) & 1) {
+                                oc[r[j]] = cc[j];
+                                ov[r[j]] = dadd(0.0, p[j]);
+                            } else {
+                                ov[r[j]] = dadd(cur[j], p[j]);
+                            }
+                        }
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -1273,40 +1337,37 @@ int hub_grid(spg_ctx* ctx) {
     static const char* g = std::getenv("SPG_HUB_CTAS");
     return ctx->num_sms * (g ? std::atoi(g) : 2);
 }
+void hub_attr(spg_ctx* ctx) {
+    static bool done[64] = {};
+    if (ctx->device < 64 && done[ctx->device]) return;
+    SPG_CUDA(cudaFuncSetAttribute(k_hub_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HubSmem)));
+    SPG_CUDA(cudaFuncSetAttribute(k_hub_num, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HubSmem)));
+    if (ctx->device < 64) done[ctx->device] = true;
+}
 
 int64_t hub_symbolic(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const int32_t* big_list, int nbig,
-                     const int64_t* prod, int32_t* drows, int64_t* side_nnz, int64_t* big_products) {
+                     const int64_t* prod, int32_t* drows, int64_t* side_nnz, uint32_t* gbm, int64_t* big_products) {
     // the rows, heaviest first (each row is one CTA's job: the long ones
-    // must not start last)
-    std::vector<int32_t> hrows(nbig);
-    SPG_CUDA(cudaMemcpyAsync(hrows.data(), big_list, nbig * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
-    SPG_CUDA(cudaStreamSynchronize(ctx->stream));
-    std::sort(hrows.begin(), hrows.end());
-    DBuf<int64_t> dprod(ctx, nbig), dnnz(ctx, nbig), sums(ctx, 2);
+    // must not start last): a device sort of (products, row) pairs
+    DBuf<int64_t> dprod(ctx, nbig), dnnz(ctx, nbig), sums(ctx, 2), pkeys(ctx, nbig);
     {
-        SPG_CUDA(cudaMemcpyAsync(drows, hrows.data(), nbig * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
-        k_side_gather<<<grid_for(ctx, nbig), 256, 0, ctx->stream>>>(drows, nbig, prod, dprod);
+        k_side_gather<<<grid_for(ctx, nbig), 256, 0, ctx->stream>>>(big_list, nbig, prod, dprod);
         SPG_LAUNCH_CHECK();
-        std::vector<int64_t> hp(nbig);
-        SPG_CUDA(cudaMemcpyAsync(hp.data(), dprod.get(), nbig * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
-        SPG_CUDA(cudaStreamSynchronize(ctx->stream));
-        std::vector<int> ord(nbig);
-        for (int r = 0; r < nbig; ++r) ord[r] = r;
-        std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return hp[x] > hp[y]; });
-        std::vector<int32_t> sorted(nbig);
-        for (int r = 0; r < nbig; ++r) sorted[r] = hrows[ord[r]];
-        hrows.swap(sorted);
-        SPG_CUDA(cudaMemcpyAsync(drows, hrows.data(), nbig * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
-        SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+        size_t tmp = 0;
+        SPG_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, dprod.get(), pkeys.get(), big_list, drows,
+                                                           nbig, 0, 64, ctx->stream));
+        DBuf<unsigned char> t(ctx, tmp);
+        SPG_CUDA(cub::DeviceRadixSort::SortPairsDescending(t.get(), tmp, dprod.get(), pkeys.get(), big_list, drows,
+                                                           nbig, 0, 64, ctx->stream));
     }
+    hub_attr(ctx);
     DBuf<unsigned> ticket(ctx, 1);
     SPG_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), ctx->stream));
     {
         KTime kt(ctx, "hub_symbolic");
-        k_hub<false><<<hub_grid(ctx), 32 * HUB_NW, 0, ctx->stream>>>(drows, nbig, a->rowptr, a->colind, a->values,
-                                                                    b->rowptr, b->colind, b->values, b->ncols,
-                                                                    ticket, nullptr, side_nnz, nullptr, nullptr,
-                                                                    nullptr);
+        k_hub_sym<<<hub_grid(ctx), 32 * HUB_NW, sizeof(HubSmem), ctx->stream>>>(drows, nbig, a->rowptr, a->colind,
+                                                                               b->rowptr, b->colind, ticket, gbm,
+                                                                               side_nnz);
         SPG_LAUNCH_CHECK();
     }
     k_side_gather<<<grid_for(ctx, nbig), 256, 0, ctx->stream>>>(drows, nbig, prod, dprod);
@@ -1325,15 +1386,14 @@ int64_t hub_symbolic(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const int
     return h[1];
 }
 
-void hub_numeric(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const int32_t* drows, int nbig, spg_csr* c) {
-    const int grid = hub_grid(ctx);
-    DBuf<double> scratch(ctx, static_cast<size_t>(grid) * HUB_W);
+void hub_numeric(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const int32_t* drows, int nbig,
+                 const uint32_t* gbm, spg_csr* c) {
     DBuf<unsigned> ticket(ctx, 1);
     SPG_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), ctx->stream));
     KTime kt(ctx, "hub_numeric");
-    k_hub<true><<<grid, 32 * HUB_NW, 0, ctx->stream>>>(drows, nbig, a->rowptr, a->colind, a->values, b->rowptr,
-                                                        b->colind, b->values, b->ncols, ticket, scratch, nullptr,
-                                                        c->rowptr, c->colind, c->values);
+    k_hub_num<<<hub_grid(ctx), 32 * HUB_NW, sizeof(HubSmem), ctx->stream>>>(
+        drows, nbig, a->rowptr, a->colind, a->values, b->rowptr, b->colind, b->values, ticket, gbm, c->rowptr,
+        c->colind, c->values);
     SPG_LAUNCH_CHECK();
 }
 
@@ -1556,10 +1616,13 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEven
     int64_t big_products = 0, big_nnz = 0;  // C capacity = products of tile rows + exact nnz of big rows
     static const char* esc_env = std::getenv("SPG_BIG_ESC");
     const bool hub = b->ncols <= HUB_MAX_COLS && !(esc_env && esc_env[0] == '1');
+    // hub path: one bitmap of HUB_W bits per BIG row (the symbolic pass's
+    // columns, read back by the numeric pass)
+    DBuf<uint32_t> gbm(ctx, (nbig && hub) ? static_cast<size_t>(nbig) * (HUB_W / 32) : 1);
     if (nbig) {
         KTime kt(ctx, "big_rows");
         if (hub)
-            big_nnz = hub_symbolic(ctx, a, b, big_list, nbig, prod, drows, side_nnz, &big_products);
+            big_nnz = hub_symbolic(ctx, a, b, big_list, nbig, prod, drows, side_nnz, gbm, &big_products);
         else
             big_nnz = big_rows_esc(ctx, a, b, big_list, nbig, prod, drows, side_cp, side_vp, side_nnz, outc, outv,
                                    hprof, &big_products);
@@ -1594,7 +1657,7 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEven
         SPG_LAUNCH_CHECK();
     }
     if (nbig && hub) {
-        hub_numeric(ctx, a, b, drows, nbig, c);
+        hub_numeric(ctx, a, b, drows, nbig, gbm, c);
     } else if (nbig) {
         KTime kt(ctx, "big_copy");
         k_big_copy<<<std::min(nbig, ctx->num_sms * 8), 256, 0, ctx->stream>>>(drows, nbig, side_cp, side_vp,
