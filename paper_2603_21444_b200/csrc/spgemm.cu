@@ -1333,9 +1333,12 @@ struct HostProf {
 // symbolic pass sizes the rows (side_nnz) for k_tile; the numeric pass runs
 // after k_tile (hub_numeric). drows receives the BIG rows in ascending order.
 constexpr int64_t HUB_MAX_COLS = HUB_W;
-int hub_grid(spg_ctx* ctx) {
+// CTAs per SM: the symbolic pass hides its latency with 2; the numeric pass
+// keeps the running sums of the rows in flight in L2, and one row per SM
+// measured best (R-MAT 18: 65.0 ms against 69.7 with 2)
+int hub_grid(spg_ctx* ctx, bool numeric) {
     static const char* g = std::getenv("SPG_HUB_CTAS");
-    return ctx->num_sms * (g ? std::atoi(g) : 2);
+    return ctx->num_sms * (g ? std::atoi(g) : (numeric ? 1 : 2));
 }
 void hub_attr(spg_ctx* ctx) {
     static bool done[64] = {};
@@ -1365,7 +1368,7 @@ int64_t hub_symbolic(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const int
     SPG_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), ctx->stream));
     {
         KTime kt(ctx, "hub_symbolic");
-        k_hub_sym<<<hub_grid(ctx), 32 * HUB_NW, sizeof(HubSmem), ctx->stream>>>(drows, nbig, a->rowptr, a->colind,
+        k_hub_sym<<<hub_grid(ctx, false), 32 * HUB_NW, sizeof(HubSmem), ctx->stream>>>(drows, nbig, a->rowptr, a->colind,
                                                                                b->rowptr, b->colind, ticket, gbm,
                                                                                side_nnz);
         SPG_LAUNCH_CHECK();
@@ -1391,7 +1394,7 @@ void hub_numeric(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const int32_t
     DBuf<unsigned> ticket(ctx, 1);
     SPG_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), ctx->stream));
     KTime kt(ctx, "hub_numeric");
-    k_hub_num<<<hub_grid(ctx), 32 * HUB_NW, sizeof(HubSmem), ctx->stream>>>(
+    k_hub_num<<<hub_grid(ctx, true), 32 * HUB_NW, sizeof(HubSmem), ctx->stream>>>(
         drows, nbig, a->rowptr, a->colind, a->values, b->rowptr, b->colind, b->values, ticket, gbm, c->rowptr,
         c->colind, c->values);
     SPG_LAUNCH_CHECK();

@@ -101,7 +101,7 @@ def main():
     ap.add_argument("--configs", default="1,2,3,4,5")
     ap.add_argument("--rmat-scale", type=int, default=22)
     ap.add_argument("--reps", type=int, default=3)
-    ap.add_argument("--batch-products", type=float, default=2.5e9)
+    ap.add_argument("--batch-products", type=float, default=6e9)
     args = ap.parse_args()
     dev = spg.Device(0)
     want = [int(x) for x in args.configs.split(",")]
