@@ -4,6 +4,7 @@
 // distributed drivers. Every multiply here runs on the B200 via the C ABI.
 // Oracle: an independent dense triple loop (ascending k, present iff a stored
 // pair contributes), as in the reference's tests/oracles.hpp:42-61.
+#include <algorithm>
 #include <cmath>
 
 #include "mini_test.hpp"
@@ -185,6 +186,53 @@ TEST_CASE("trident and SUMMA reproduce the serial product") {
     const CsrMatrix rt = transpose(r);
     const DriverResult dr = trident_spgemm(r, rt, TridentGrid::create(8, 2), TopologySpec::preset(0, 2));
     CHECK(allclose(dr.c, spgemm_local(r, rt), 1e-12));
+}
+
+TEST_CASE("to_jsonl writes the reference's schema (host only)") {
+    EventTimeline tl;
+    tl.events.push_back({EventType::enqueue_request, 3, 1, 0, Operand::A, LinkClass::GI, 0.5, 0.5, 0, 0});
+    tl.events.push_back({EventType::transfer_complete, 1, 3, 1, Operand::B, LinkClass::LI, 0.25, 1.0, 42, 540});
+    tl.events.push_back({EventType::allgather_complete, 2, -1, 1, Operand::B, LinkClass::LI, 0.0, 2.0, 7, 96});
+    const std::string want =
+        "{\"type\":\"enqueue-request\",\"actors\":[3,1],\"round\":0,\"t_start\":0.5,\"t_end\":0.5,\"bytes\":0,"
+        "\"operand\":\"A\",\"link\":\"GI\",\"nnz\":0}\n"
+        "{\"type\":\"transfer-complete\",\"actors\":[1,3],\"round\":1,\"t_start\":0.25,\"t_end\":1.0,\"bytes\":540,"
+        "\"operand\":\"B\",\"link\":\"LI\",\"nnz\":42}\n"
+        "{\"type\":\"allgather-complete\",\"actors\":[2,-1],\"round\":1,\"t_start\":0.0,\"t_end\":2.0,\"bytes\":96,"
+        "\"operand\":\"B\",\"link\":\"LI\",\"nnz\":7}\n";
+    CHECK(tl.to_jsonl() == want);
+}
+
+TEST_CASE("trident timeline: the reference's event counts; node_start_delay delays a node") {
+    const CsrMatrix a = gen_erdos_renyi(400, 0.02, 5), b = gen_erdos_renyi(400, 0.02, 6);
+    const TridentGrid g = TridentGrid::create(8, 2);
+    const DriverResult r = trident_spgemm(a, b, g, TopologySpec::preset(0, 2), {0.0, 0.03, 0.0, 0.0});
+    CHECK(r.c == spgemm_local(a, b));  // the rounds run as one k-ordered multiply
+    // expected counts from the schedule (engine.cpp:228-302): a request, a
+    // serve and a transfer per remote A tile and per remote own-index B slice,
+    // one allgather per node and round, one compute per rank and round
+    const TridentSchedule sch(g.q);
+    int remote = 0;
+    for (int rank = 0; rank < g.procs; ++rank) {
+        const auto c = g.coords_of(rank);
+        for (int rd = 0; rd < g.q; ++rd) {
+            remote += sch.a_owner(g, c.i, c.j, c.k, rd) != rank;
+            remote += sch.b_owner(g, c.i, c.j, c.k, rd) != rank;
+        }
+    }
+    int n[5] = {0, 0, 0, 0, 0};
+    double first_late = 1e9;
+    for (const auto& e : r.timeline.events) {
+        n[static_cast<int>(e.type)]++;
+        if (e.type == EventType::transfer_complete && e.dst / 2 == 1) first_late = std::min(first_late, e.t_start);
+    }
+    CHECK(n[0] == remote && n[1] == remote && n[2] == remote);
+    CHECK(n[3] == (g.procs / g.gpus_per_node) * g.q);
+    CHECK(n[4] == g.procs * g.q);
+    CHECK(first_late >= 0.03);
+    const std::string j = r.timeline.to_jsonl();
+    CHECK(static_cast<std::size_t>(std::count(j.begin(), j.end(), '\n')) == r.timeline.events.size());
+    CHECK_THROWS_AS(trident_spgemm(a, b, g, TopologySpec::preset(0, 2), {-1.0}), ParameterError);
 }
 
 int main(int argc, char** argv) { return mini::run_all(argc > 1 ? argv[1] : nullptr); }
