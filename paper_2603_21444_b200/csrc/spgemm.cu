@@ -123,7 +123,7 @@ __host__ __device__ __forceinline__ bool tile_small(int64_t p, int64_t ne) {
 __global__ void k_row_prep(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
                            const int64_t* __restrict__ brp, int64_t m, int64_t* __restrict__ prod,
                            int64_t* __restrict__ wt, int8_t* __restrict__ kind, uint64_t* __restrict__ espan,
-                           int32_t* __restrict__ big_rows, int32_t* __restrict__ nbig) {
+                           int32_t* __restrict__ big_rows, int32_t* __restrict__ nbig, bool medium_big) {
     // half-warp per row (two rows in flight per warp: the row is a chain of
     // dependent loads arp -> acol -> brp); loops are warp-uniform
     const int lane = threadIdx.x & 31, sub = lane & 15, half = lane >> 4;
@@ -164,7 +164,7 @@ __global__ void k_row_prep(const int64_t* __restrict__ arp, const int32_t* __res
         for (int o = 8; o > 0; o >>= 1) maxlen = max(maxlen, static_cast<int64_t>(__shfl_xor_sync(FULL, maxlen, o)));
         int8_t rk = RK_BIG;
         if (tile_small(p, ne)) rk = RK_SMALL;
-        else if (tile_weight(p, ne) <= tile::PMAX && maxlen <= tile::SP_LEN_MAX) rk = RK_MEDIUM;
+        else if (!medium_big && tile_weight(p, ne) <= tile::PMAX && maxlen <= tile::SP_LEN_MAX) rk = RK_MEDIUM;
         const uint64_t pr = static_cast<uint64_t>(p);
         const bool spans = ok && rk != RK_BIG;
         {  // rows of <= 32 entries: in-row product offsets from registers
@@ -1572,6 +1572,10 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEven
     HostProf hprof;
     const int64_t m = a->nrows, n = b->ncols;
     const int cshift = cshift_for(n);
+    // BIG rows (and, with the hub path, MEDIUM rows too: single-row tiles whose
+    // cost varies 10x stall k_tile's look-back chain) go to the side path
+    static const char* esc_env = std::getenv("SPG_BIG_ESC");
+    const bool hub = b->ncols <= HUB_MAX_COLS && !(esc_env && esc_env[0] == '1');
     // 1: products, entry spans, row weights, BIG-row list
     DBuf<int64_t> prod(ctx, m), wt(ctx, m), total(ctx, 1);
     DBuf<int8_t> kind(ctx, m);
@@ -1581,7 +1585,7 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEven
     {
         KTime kt(ctx, "row_prep");
         k_row_prep<<<grid_for(ctx, 32 * m), 256, 0, ctx->stream>>>(a->rowptr, a->colind, b->rowptr, m, prod, wt,
-                                                                   kind, espan, big_list, nbig_d);
+                                                                   kind, espan, big_list, nbig_d, hub);
         SPG_LAUNCH_CHECK();
     }
     {
@@ -1617,8 +1621,7 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEven
     std::vector<std::unique_ptr<DBuf<int32_t>>> outc;
     std::vector<std::unique_ptr<DBuf<double>>> outv;
     int64_t big_products = 0, big_nnz = 0;  // C capacity = products of tile rows + exact nnz of big rows
-    static const char* esc_env = std::getenv("SPG_BIG_ESC");
-    const bool hub = b->ncols <= HUB_MAX_COLS && !(esc_env && esc_env[0] == '1');
+
     // hub path: one bitmap of HUB_W bits per BIG row (the symbolic pass's
     // columns, read back by the numeric pass)
     DBuf<uint32_t> gbm(ctx, (nbig && hub) ? static_cast<size_t>(nbig) * (HUB_W / 32) : 1);
