@@ -506,10 +506,17 @@ __global__ void k_big_finish(const int32_t* __restrict__ rows, int nrows, const 
 //    reference's acc[j] += av*bv. The running sums live in the row's own C
 //    range (compact, L2-resident), not in a dense scratch.
 constexpr int HUB_NW = 8, HUB_RANGE = 32768, HUB_W = HUB_NW * HUB_RANGE, HUB_WORDS = HUB_RANGE / 32;
+constexpr int HUB_ACC = 1536;  // running sums a warp keeps in shared memory
+struct HubSymSmem {
+    uint32_t bm[HUB_NW][HUB_WORDS];  // the row's columns
+    int64_t cnt[HUB_NW];
+    int row;
+};
 struct HubSmem {
+    double acc[HUB_NW][HUB_ACC];     // running sums at their rank (warps with <= HUB_ACC columns)
     uint32_t sb[HUB_NW][HUB_WORDS];  // the row's columns (symbolic bitmap)
     uint32_t sp[HUB_NW][HUB_WORDS];  // exclusive prefix of the words' popcounts
-    uint32_t bm[HUB_NW][HUB_WORDS];  // touched so far (numeric)
+    uint32_t bm[HUB_NW][HUB_WORDS];  // touched so far
     int64_t cnt[HUB_NW];
     int row;
 };
@@ -548,7 +555,7 @@ __global__ void __launch_bounds__(32 * HUB_NW) k_hub_sym(const int32_t* __restri
                                                          const int32_t* __restrict__ bcol, unsigned* __restrict__ ticket,
                                                          uint32_t* __restrict__ gbm, int64_t* __restrict__ side_nnz) {
     extern __shared__ __align__(16) unsigned char hub_raw[];
-    HubSmem& S = *reinterpret_cast<HubSmem*>(hub_raw);
+    HubSymSmem& S = *reinterpret_cast<HubSymSmem*>(hub_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t* my = S.bm[warp];
     const int64_t lo_c = int64_t(warp) * HUB_RANGE, hi_c = lo_c + HUB_RANGE;
@@ -644,6 +651,11 @@ __global__ void __launch_bounds__(32 * HUB_NW) k_hub_num(const int32_t* __restri
         for (int w = 0; w < warp; ++w) base += S.cnt[w];
         int32_t* oc = ccol + base;
         double* ov = cval + base;
+        // the running sums: in shared memory when the warp's columns fit, else
+        // in place in C (L2)
+        const uint32_t nw = __shfl_sync(FULL, winc, 31);
+        const bool smacc = nw <= static_cast<uint32_t>(HUB_ACC);
+        double* acc = smacc ? S.acc[warp] : ov;
         for (int64_t c0 = e0; c0 < e1; c0 += 32) {
             int64_t s, f;
             double av;
@@ -676,21 +688,23 @@ __global__ void __launch_bounds__(32 * HUB_NW) k_hub_num(const int32_t* __restri
                         }
                     }
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) cur[j] = (r[j] >= 0 && !((first >> j) & 1)) ? ov[r[j]] : 0.0;
+                    for (int j = 0; j < 4; ++j) cur[j] = (r[j] >= 0 && !((first >> j) & 1)) ? acc[r[j]] : 0.0;
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
                         if (r[j] >= 0) {
                             if ((first >> j) & 1) {
                                 oc[r[j]] = cc[j];
-                                ov[r[j]] = dadd(0.0, p[j]);
+                                acc[r[j]] = dadd(0.0, p[j]);
                             } else {
-                                ov[r[j]] = dadd(cur[j], p[j]);
+                                acc[r[j]] = dadd(cur[j], p[j]);
                             }
                         }
                 }
                 __syncwarp();
             }
         }
+        if (smacc)
+            for (uint32_t x = lane; x < nw; x += 32) ov[x] = acc[x];
         __syncthreads();
     }
 }
@@ -1338,12 +1352,12 @@ constexpr int64_t HUB_MAX_COLS = HUB_W;
 // measured best (R-MAT 18: 65.0 ms against 69.7 with 2)
 int hub_grid(spg_ctx* ctx, bool numeric) {
     static const char* g = std::getenv("SPG_HUB_CTAS");
-    return ctx->num_sms * (g ? std::atoi(g) : (numeric ? 1 : 2));
+    return ctx->num_sms * (g ? std::atoi(g) : (numeric ? 1 : 6));
 }
 void hub_attr(spg_ctx* ctx) {
     static bool done[64] = {};
     if (ctx->device < 64 && done[ctx->device]) return;
-    SPG_CUDA(cudaFuncSetAttribute(k_hub_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HubSmem)));
+    SPG_CUDA(cudaFuncSetAttribute(k_hub_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HubSymSmem)));
     SPG_CUDA(cudaFuncSetAttribute(k_hub_num, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HubSmem)));
     if (ctx->device < 64) done[ctx->device] = true;
 }
@@ -1368,7 +1382,7 @@ int64_t hub_symbolic(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const int
     SPG_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), ctx->stream));
     {
         KTime kt(ctx, "hub_symbolic");
-        k_hub_sym<<<hub_grid(ctx, false), 32 * HUB_NW, sizeof(HubSmem), ctx->stream>>>(drows, nbig, a->rowptr, a->colind,
+        k_hub_sym<<<hub_grid(ctx, false), 32 * HUB_NW, sizeof(HubSymSmem), ctx->stream>>>(drows, nbig, a->rowptr, a->colind,
                                                                                b->rowptr, b->colind, ticket, gbm,
                                                                                side_nnz);
         SPG_LAUNCH_CHECK();
