@@ -309,3 +309,68 @@ def test_repeated_multiplies_are_identical(dev, which):
     for _ in range(12):
         c = dev.spgemm(da, db).download()
         assert same(c, ref)
+
+
+def _hub_case(ncols, seed):
+    """A mix the hub path must get right: rows with thousands of entries over
+    long and short B rows, a row whose products all hit one column (a bucket
+    of thousands in k_tile terms), rows that reach the last column of the
+    window, and ordinary rows."""
+    rng = np.random.default_rng(seed)
+    nb = 3000
+    # B: mostly short rows, some long ones, a few spanning the whole width
+    lens = rng.integers(0, 12, nb)
+    lens[rng.choice(nb, 40, replace=False)] = rng.integers(200, 2000, 40)
+    lens = np.minimum(lens, ncols)
+    b_rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    b_ci = np.concatenate([np.sort(rng.choice(ncols, int(l), replace=False)) for l in lens]).astype(np.int64)
+    b_ci[b_rp[5]:b_rp[6]] = np.arange(ncols - lens[5], ncols) if lens[5] else b_ci[b_rp[5]:b_rp[6]]
+    b_va = rng.uniform(-1, 1, int(b_rp[-1]))
+    b = O.Csr(nb, ncols, b_rp, b_ci, b_va)
+    rows = [np.sort(rng.choice(nb, 1500, replace=False)),          # a hub row over long and short B rows
+            np.sort(rng.choice(nb, 400, replace=False)),
+            np.array([5, 6, 7]),                                    # reaches the last column
+            np.sort(rng.choice(nb, 8, replace=False)),              # an ordinary row
+            np.arange(0, 2500, 3)]
+    a_rp = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    a_ci = np.concatenate(rows).astype(np.int64)
+    a = O.Csr(len(rows), nb, a_rp, a_ci, rng.uniform(-2, 2, len(a_ci)))
+    return a, b
+
+
+@pytest.mark.parametrize("ncols", [1000, 262144, 262145])
+@pytest.mark.parametrize("seed", [1, 2])
+def test_hub_rows_bit_exact(dev, ncols, seed):
+    """BIG and MEDIUM rows: the dense hub accumulator (B up to 2^18 columns)
+    and the sort-based ESC (wider B) against the oracle, bit-exact; 262144 is
+    the widest B the hub takes, 262145 the narrowest that goes to the ESC."""
+    a, b = _hub_case(ncols, seed)
+    assert same(gpu_mul(dev, a, b), O.port_spgemm(a, b))
+
+
+def test_hub_and_esc_agree(dev):
+    """The same hub-path product through both side paths (SPG_BIG_ESC=1 is
+    read once per process, so the ESC run is a child process)."""
+    import subprocess
+    import sys
+    code = """
+import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)
+import numpy as np, oracle as O, paper_2603_21444_b200 as spg
+from test_gpu_parity import _hub_case
+a, b = _hub_case(5000, 3)
+d = spg.Device(0)
+c = d.spgemm(d.upload(a), d.upload(b)).download()
+np.save(%r, np.concatenate([np.asarray(c.rowptr, np.float64), np.asarray(c.colind, np.float64), np.asarray(c.values)]))
+"""
+    import os
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for esc in ("0", "1"):
+        f = os.path.join(tempfile.mkdtemp(), "c.npy")
+        env = dict(os.environ, SPG_BIG_ESC=esc)
+        r = subprocess.run([sys.executable, "-c", code % (root, os.path.join(root, "tests"), f)], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
