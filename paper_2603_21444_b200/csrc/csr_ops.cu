@@ -652,6 +652,15 @@ spg_csr* copy_csr(spg_ctx* ctx, const spg_csr* s) {
     return c;
 }
 
+// A slice that lives in this device's own memory is copied by the SMs (HBM
+// bound), so that the copy engines are left to the peer pulls: a local
+// device-to-device copy on a copy engine competes with the NVLink pulls of the
+// other slices.
+template <typename T>
+__global__ void k_copy_elems(const T* __restrict__ src, T* __restrict__ dst, int64_t n) {
+    GRID_STRIDE(i, n) dst[i] = src[i];
+}
+
 spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n, cudaEvent_t rp_ready,
                  std::vector<SlicePull>* log) {
     if (n == 0) {
@@ -668,14 +677,21 @@ spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n, cudaEvent_t 
     }
     spg_csr* out = new_csr(ctx, rows, ncols, nnz);
     SPG_CUDA(cudaMemsetAsync(out->rowptr, 0, sizeof(int64_t), ctx->stream));
-    if (n > 1 && ctx->aux[0]) SPG_CUDA(cudaEventRecord(ctx->aux_ev[spg_ctx::NAUX], ctx->stream));  // fork point
-    int64_t r = 0, base = 0;
+    const bool fork = n > 1 && ctx->aux[0];
+    if (fork) SPG_CUDA(cudaEventRecord(ctx->aux_ev[spg_ctx::NAUX], ctx->stream));  // fork point
     const int dd = ctx->device;
     if (log) log->assign(n, SlicePull{});
+    // 1: the column/value pulls first (one aux stream per slice, concurrently
+    // on the copy engines; local slices by the SMs)
+    int64_t base = 0;
     for (int s = 0; s < n; ++s) {
         const spg_csr* sl = slices[s];
         const int sd = sl->ctx->device;
-        const int64_t* rp = sl->rowptr;
+        cudaStream_t st = ctx->stream;
+        if (fork) {
+            st = ctx->aux[s % spg_ctx::NAUX];
+            if (s < spg_ctx::NAUX) SPG_CUDA(cudaStreamWaitEvent(st, ctx->aux_ev[spg_ctx::NAUX], 0));
+        }
         if (log) {
             SlicePull& L = (*log)[s];
             L.rows = sl->nrows;
@@ -683,42 +699,43 @@ spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n, cudaEvent_t 
             L.dev_bytes = (sl->nrows + 1) * int64_t(sizeof(int64_t)) + sl->nnz * int64_t(sizeof(int32_t) + sizeof(double));
             L.t0 = ctx->timer.ev();
             L.t1 = ctx->timer.ev();
-            SPG_CUDA(cudaEventRecord(L.t0, ctx->stream));
-        }
-        DBuf<int64_t> tmp(ctx, sd == dd ? 0 : sl->nrows + 1);
-        if (sd != dd) {
-            SPG_CUDA(cudaMemcpyPeerAsync(tmp.get(), dd, sl->rowptr, sd, (sl->nrows + 1) * sizeof(int64_t), ctx->stream));
-            rp = tmp.get();
-        }
-        if (sl->nrows) {
-            KTime kt(ctx, "vconcat_rebase");
-            k_rebase_rowptr<<<grid_for(ctx, sl->nrows), 256, 0, ctx->stream>>>(rp, sl->nrows, base, out->rowptr + r + 1);
-            SPG_LAUNCH_CHECK();
+            SPG_CUDA(cudaEventRecord(L.t0, st));
         }
         if (sl->nnz) {
-            // slices are pulled concurrently by the copy engines (one aux stream
-            // each, forked from and joined back into the context stream)
-            cudaStream_t st = ctx->stream;
-            if (n > 1 && ctx->aux[0]) {
-                st = ctx->aux[s % spg_ctx::NAUX];
-                if (s < spg_ctx::NAUX) SPG_CUDA(cudaStreamWaitEvent(st, ctx->aux_ev[spg_ctx::NAUX], 0));
-            }
-            if (sd == dd) {
+            const bool own = sd == dd && sl->storage != 2;  // this device's memory (not an IPC view)
+            if (own) {
+                k_copy_elems<int32_t><<<grid_for(ctx, sl->nnz), 256, 0, st>>>(sl->colind, out->colind + base, sl->nnz);
+                SPG_LAUNCH_CHECK();
+                k_copy_elems<double><<<grid_for(ctx, sl->nnz), 256, 0, st>>>(sl->values, out->values + base, sl->nnz);
+                SPG_LAUNCH_CHECK();
+            } else if (sd == dd) {
                 SPG_CUDA(cudaMemcpyAsync(out->colind + base, sl->colind, sl->nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
                 SPG_CUDA(cudaMemcpyAsync(out->values + base, sl->values, sl->nnz * sizeof(double), cudaMemcpyDeviceToDevice, st));
             } else {
                 SPG_CUDA(cudaMemcpyPeerAsync(out->colind + base, dd, sl->colind, sd, sl->nnz * sizeof(int32_t), st));
                 SPG_CUDA(cudaMemcpyPeerAsync(out->values + base, dd, sl->values, sd, sl->nnz * sizeof(double), st));
             }
-            if (log) SPG_CUDA(cudaEventRecord((*log)[s].t1, st));
-        } else if (log) {
-            SPG_CUDA(cudaEventRecord((*log)[s].t1, ctx->stream));
+        }
+        if (log) SPG_CUDA(cudaEventRecord((*log)[s].t1, st));
+        base += sl->nnz;
+    }
+    // 2: the row pointers, rebased by kernels reading every slice's row
+    // pointers in place (peer access / IPC mapping: no staging copy)
+    int64_t r = 0;
+    base = 0;
+    for (int s = 0; s < n; ++s) {
+        const spg_csr* sl = slices[s];
+        if (sl->nrows) {
+            KTime kt(ctx, "vconcat_rebase");
+            k_rebase_rowptr<<<grid_for(ctx, sl->nrows), 256, 0, ctx->stream>>>(sl->rowptr, sl->nrows, base,
+                                                                                 out->rowptr + r + 1);
+            SPG_LAUNCH_CHECK();
         }
         r += sl->nrows;
         base += sl->nnz;
     }
     if (rp_ready) SPG_CUDA(cudaEventRecord(rp_ready, ctx->stream));
-    if (n > 1 && ctx->aux[0])
+    if (fork)
         for (int i = 0; i < std::min(n, spg_ctx::NAUX); ++i) {
             SPG_CUDA(cudaEventRecord(ctx->aux_ev[i], ctx->aux[i]));
             SPG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[i], 0));

@@ -1,0 +1,98 @@
+// Dev tool: pull bandwidth from peer GPUs over NVLink, copy engines vs an
+// SM-driven pull kernel (16-byte coalesced loads of the peer's memory).
+// usage: peer_bench [MB per peer]   (uses every visible GPU: GPU 0 pulls from
+// each of the others at once, like a trident rank pulling its B slices)
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#define CK(x)                                                                                   \
+    do {                                                                                        \
+        cudaError_t e = (x);                                                                    \
+        if (e != cudaSuccess) {                                                                 \
+            printf("%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e));                    \
+            exit(1);                                                                            \
+        }                                                                                       \
+    } while (0)
+
+__global__ void pull(const int4* __restrict__ src, int4* __restrict__ dst, size_t n) {
+    size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x, st = size_t(gridDim.x) * blockDim.x;
+    for (; i + 3 * st < n; i += 4 * st) {
+        int4 a = src[i], b = src[i + st], c = src[i + 2 * st], d = src[i + 3 * st];
+        dst[i] = a;
+        dst[i + st] = b;
+        dst[i + 2 * st] = c;
+        dst[i + 3 * st] = d;
+    }
+    for (; i < n; i += st) dst[i] = src[i];
+}
+
+int main(int argc, char** argv) {
+    const size_t mb = argc > 1 ? atoi(argv[1]) : 200;
+    const size_t bytes = mb << 20;
+    int ng = 0;
+    CK(cudaGetDeviceCount(&ng));
+    printf("GPUs %d, %zu MB per peer\n", ng, mb);
+    if (ng < 2) return 0;
+    std::vector<void*> src(ng);
+    for (int d = 1; d < ng; ++d) {
+        CK(cudaSetDevice(d));
+        CK(cudaMalloc(&src[d], bytes));
+        CK(cudaMemset(src[d], d, bytes));
+    }
+    CK(cudaSetDevice(0));
+    for (int d = 1; d < ng; ++d) {
+        int ok = 0;
+        CK(cudaDeviceCanAccessPeer(&ok, 0, d));
+        if (ok) cudaDeviceEnablePeerAccess(d, 0);
+    }
+    std::vector<void*> dst(ng);
+    std::vector<cudaStream_t> st(ng);
+    for (int d = 1; d < ng; ++d) {
+        CK(cudaMalloc(&dst[d], bytes));
+        CK(cudaStreamCreateWithFlags(&st[d], cudaStreamNonBlocking));
+    }
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    for (int npeer = 1; npeer < ng; ++npeer) {
+        for (int mode = 0; mode < 3; ++mode) {
+            float best = 1e9;
+            for (int it = 0; it < 5; ++it) {
+                CK(cudaDeviceSynchronize());
+                CK(cudaEventRecord(a, 0));
+                for (int d = 1; d <= npeer; ++d) {
+                    CK(cudaStreamWaitEvent(st[d], a, 0));
+                    if (mode == 0) {
+                        CK(cudaMemcpyPeerAsync(dst[d], 0, src[d], d, bytes, st[d]));
+                    } else if (mode == 1) {  // two copies per peer (two engines)
+                        CK(cudaMemcpyPeerAsync(dst[d], 0, src[d], d, bytes / 2, st[d]));
+                        CK(cudaMemcpyPeerAsync((char*)dst[d] + bytes / 2, 0, (char*)src[d] + bytes / 2, d, bytes / 2, 0));
+                    } else {
+                        pull<<<sms * 4 / npeer, 512, 0, st[d]>>>((const int4*)src[d], (int4*)dst[d], bytes / 16);
+                    }
+                    CK(cudaGetLastError());
+                }
+                for (int d = 1; d <= npeer; ++d) {
+                    cudaEvent_t ev;
+                    CK(cudaEventCreate(&ev));
+                    CK(cudaEventRecord(ev, st[d]));
+                    CK(cudaStreamWaitEvent(0, ev, 0));
+                }
+                CK(cudaEventRecord(b, 0));
+                CK(cudaEventSynchronize(b));
+                float ms;
+                CK(cudaEventElapsedTime(&ms, a, b));
+                if (it && ms < best) best = ms;
+            }
+            const char* nm[] = {"copy engine", "copy engine x2", "SM pull kernel"};
+            printf("peers %d  %-15s  %8.3f ms  %7.1f GB/s into GPU 0\n", npeer, nm[mode], best,
+                   npeer * bytes / (best * 1e-3) / 1e9);
+        }
+    }
+    return 0;
+}
