@@ -4,6 +4,7 @@
 // each of the others at once, like a trident rank pulling its B slices)
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -92,6 +93,49 @@ int main(int argc, char** argv) {
             const char* nm[] = {"copy engine", "copy engine x2", "SM pull kernel"};
             printf("peers %d  %-15s  %8.3f ms  %7.1f GB/s into GPU 0\n", npeer, nm[mode], best,
                    npeer * bytes / (best * 1e-3) / 1e9);
+        }
+    }
+    // all-to-all: every GPU pulls bytes from each other GPU at once (the
+    // trident exchange at q = 1: every rank pulls its node-mates' slices)
+    {
+        std::vector<std::vector<void*>> dd(ng, std::vector<void*>(ng, nullptr));
+        std::vector<void*> sb(ng);
+        std::vector<std::vector<cudaStream_t>> ss(ng, std::vector<cudaStream_t>(ng));
+        for (int g = 0; g < ng; ++g) {
+            CK(cudaSetDevice(g));
+            for (int h = 0; h < ng; ++h)
+                if (h != g) {
+                    int ok = 0;
+                    CK(cudaDeviceCanAccessPeer(&ok, g, h));
+                    if (ok) cudaDeviceEnablePeerAccess(h, 0);
+                    CK(cudaMalloc(&dd[g][h], bytes));
+                    CK(cudaStreamCreateWithFlags(&ss[g][h], cudaStreamNonBlocking));
+                }
+            CK(cudaMalloc(&sb[g], bytes));
+            CK(cudaMemset(sb[g], g, bytes));
+        }
+        for (int it = 0; it < 4; ++it) {
+            for (int g = 0; g < ng; ++g) {
+                CK(cudaSetDevice(g));
+                CK(cudaDeviceSynchronize());
+            }
+            cudaEvent_t e0, e1;
+            CK(cudaSetDevice(0));
+            CK(cudaEventCreate(&e0));
+            CK(cudaEventCreate(&e1));
+            auto t0 = std::chrono::high_resolution_clock::now();
+            for (int g = 0; g < ng; ++g) {
+                CK(cudaSetDevice(g));
+                for (int h = 0; h < ng; ++h)
+                    if (h != g) CK(cudaMemcpyPeerAsync(dd[g][h], g, sb[h], h, bytes, ss[g][h]));
+            }
+            for (int g = 0; g < ng; ++g) {
+                CK(cudaSetDevice(g));
+                CK(cudaDeviceSynchronize());
+            }
+            const double ms = std::chrono::duration<double, std::milli>(std::chrono::high_resolution_clock::now() - t0).count();
+            if (it) printf("all-to-all %d GPUs: %8.3f ms (host clock)  %7.1f GB/s into each GPU\n", ng, ms,
+                           (ng - 1) * bytes / (ms * 1e-3) / 1e9);
         }
     }
     return 0;
