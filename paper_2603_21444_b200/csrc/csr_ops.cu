@@ -661,6 +661,74 @@ __global__ void k_copy_elems(const T* __restrict__ src, T* __restrict__ dst, int
     GRID_STRIDE(i, n) dst[i] = src[i];
 }
 
+// Contiguous copy by the TMA engine (cp.async.bulk): each CTA moves chunks of
+// BULK_CH bytes global -> shared (completion on an mbarrier's transaction
+// count) -> global (bulk group), double-buffered; src and dst 16-byte
+// aligned, bytes a multiple of 16 (the caller copies the tail).
+constexpr int BULK_CH = 16384;
+__global__ void __launch_bounds__(32) k_bulk_copy(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst,
+                                                  int64_t bytes) {
+    __shared__ __align__(128) unsigned char buf[2][BULK_CH];
+    __shared__ __align__(8) uint64_t bar[2];
+    if (threadIdx.x != 0) return;
+    const uint32_t b0 = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[0]));
+    const uint32_t b1 = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[1]));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b0) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b1) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    unsigned ph[2] = {0u, 0u};
+    int k = 0;
+    for (int64_t off = int64_t(blockIdx.x) * BULK_CH; off < bytes; off += int64_t(gridDim.x) * BULK_CH, k ^= 1) {
+        const uint32_t n = static_cast<uint32_t>(min(int64_t(BULK_CH), bytes - off));
+        const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(buf[k]));
+        const uint32_t bk = k ? b1 : b0;
+        // the store that last read buf[k] (two chunks ago) must be done
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bk), "r"(n) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sb),
+                     "l"(src + off), "r"(n), "r"(bk)
+                     : "memory");
+        uint32_t done = 0;
+        while (!done) {
+            asm volatile(
+                "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                : "=r"(done)
+                : "r"(bk), "r"(ph[k])
+                : "memory");
+        }
+        ph[k] ^= 1u;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + off), "r"(sb), "r"(n)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// dst[0, n) = src[0, n) on stream st: by the TMA engine when src and dst are
+// 16-byte co-aligned (the unaligned tail by a small element kernel), else by
+// the SMs.
+template <typename T>
+void device_copy(spg_ctx* ctx, cudaStream_t st, T* dst, const T* src, int64_t n) {
+    if (n <= 0) return;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src), b = reinterpret_cast<uintptr_t>(dst);
+    const int64_t bytes = n * static_cast<int64_t>(sizeof(T));
+    if ((a % 16) == 0 && (b % 16) == 0 && bytes >= 16) {
+        const int64_t body = bytes & ~int64_t(15);
+        const int g = static_cast<int>(std::min<int64_t>((body + BULK_CH - 1) / BULK_CH, int64_t(ctx->num_sms) * 4));
+        k_bulk_copy<<<g, 32, 0, st>>>(reinterpret_cast<const unsigned char*>(src), reinterpret_cast<unsigned char*>(dst),
+                                      body);
+        SPG_LAUNCH_CHECK();
+        const int64_t done = body / static_cast<int64_t>(sizeof(T));
+        if (done < n) {
+            k_copy_elems<T><<<1, 32, 0, st>>>(src + done, dst + done, n - done);
+            SPG_LAUNCH_CHECK();
+        }
+        return;
+    }
+    k_copy_elems<T><<<grid_for(ctx, n), 256, 0, st>>>(src, dst, n);
+    SPG_LAUNCH_CHECK();
+}
+
 spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n, cudaEvent_t rp_ready,
                  std::vector<SlicePull>* log) {
     if (n == 0) {
@@ -704,10 +772,8 @@ spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n, cudaEvent_t 
         if (sl->nnz) {
             const bool own = sd == dd && sl->storage != 2;  // this device's memory (not an IPC view)
             if (own) {
-                k_copy_elems<int32_t><<<grid_for(ctx, sl->nnz), 256, 0, st>>>(sl->colind, out->colind + base, sl->nnz);
-                SPG_LAUNCH_CHECK();
-                k_copy_elems<double><<<grid_for(ctx, sl->nnz), 256, 0, st>>>(sl->values, out->values + base, sl->nnz);
-                SPG_LAUNCH_CHECK();
+                device_copy(ctx, st, out->colind + base, sl->colind, sl->nnz);
+                device_copy(ctx, st, out->values + base, sl->values, sl->nnz);
             } else if (sd == dd) {
                 SPG_CUDA(cudaMemcpyAsync(out->colind + base, sl->colind, sl->nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
                 SPG_CUDA(cudaMemcpyAsync(out->values + base, sl->values, sl->nnz * sizeof(double), cudaMemcpyDeviceToDevice, st));
