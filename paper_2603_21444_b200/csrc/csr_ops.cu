@@ -11,6 +11,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <climits>
+#include <cstdlib>
 
 #include "block_scan.cuh"
 #include "spg_internal.cuh"
@@ -729,6 +730,43 @@ void device_copy(spg_ctx* ctx, cudaStream_t st, T* dst, const T* src, int64_t n)
     SPG_LAUNCH_CHECK();
 }
 
+// Slices in peers' memory (peer access or IPC mappings): with three or more
+// of them pulled at once (N=4 at q = 1: an all-to-all) the SMs pull them —
+// each thread keeps 8 independent NVLink loads in flight, column indices
+// first, then values; SM pulls reach 580-640 GB/s into each of 4 GPUs in an
+// all-to-all against 402 for the copy engines, at any element width
+// (`scripts/peer_bench.cu`, `profiles/r2r_*`). With one or two peers the copy
+// engines are faster (one puller: 790 against 717 GB/s; N=2 step 12.84 ms
+// against 13.23). The SM pulls of all slices together take SPG_PULL_BLOCKS
+// (default 2) 512-thread CTAs per SM, so that the multiply's row preparation
+// still finds room beside them. SPG_PULL_CE=1 / 0 forces copy engines / SMs.
+template <typename T>
+__device__ __forceinline__ void pull_elems(const T* __restrict__ src, T* __restrict__ dst, int64_t n) {
+    constexpr int U = 8;
+    const int64_t st = int64_t(gridDim.x) * blockDim.x;
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (; i + (U - 1) * st < n; i += U * st) {
+        T r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) r[u] = src[i + u * st];
+#pragma unroll
+        for (int u = 0; u < U; ++u) dst[i + u * st] = r[u];
+    }
+    for (; i < n; i += st) dst[i] = src[i];
+}
+
+__global__ void __launch_bounds__(512) k_pull_slice(const int32_t* __restrict__ sc, int32_t* __restrict__ dc,
+                                                    const double* __restrict__ sv, double* __restrict__ dv,
+                                                    int64_t nnz) {
+    pull_elems(sc, dc, nnz);
+    pull_elems(sv, dv, nnz);
+}
+
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e && *e ? std::atoi(e) : dflt;
+}
+
 spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n, cudaEvent_t rp_ready,
                  std::vector<SlicePull>* log) {
     if (n == 0) {
@@ -749,9 +787,32 @@ spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n, cudaEvent_t 
     if (fork) SPG_CUDA(cudaEventRecord(ctx->aux_ev[spg_ctx::NAUX], ctx->stream));  // fork point
     const int dd = ctx->device;
     if (log) log->assign(n, SlicePull{});
-    // 1: the column/value pulls first (one aux stream per slice, concurrently
-    // on the copy engines; local slices by the SMs)
-    int64_t base = 0;
+    // 1: the row pointers, rebased by kernels reading every slice's row
+    // pointers in place (peer access / IPC mapping: no staging copy); issued
+    // first so that they are not queued behind the pulls
+    int64_t r = 0, base = 0;
+    for (int s = 0; s < n; ++s) {
+        const spg_csr* sl = slices[s];
+        if (sl->nrows) {
+            KTime kt(ctx, "vconcat_rebase");
+            k_rebase_rowptr<<<grid_for(ctx, sl->nrows), 256, 0, ctx->stream>>>(sl->rowptr, sl->nrows, base,
+                                                                                 out->rowptr + r + 1);
+            SPG_LAUNCH_CHECK();
+        }
+        r += sl->nrows;
+        base += sl->nnz;
+    }
+    if (rp_ready) SPG_CUDA(cudaEventRecord(rp_ready, ctx->stream));
+    // 2: the column/value pulls (one aux stream per slice, concurrently; local
+    // slices by the SMs)
+    int remote = 0;  // slices pulled from a peer: they share the pull CTAs
+    for (int s = 0; s < n; ++s)
+        remote += slices[s]->nnz && (slices[s]->ctx->device != dd || slices[s]->storage == 2);
+    static const int pull_ce_env = env_int("SPG_PULL_CE", -1);
+    const bool pull_ce = pull_ce_env == 1 || (pull_ce_env != 0 && remote < 3);
+    static const int pull_per_sm = std::max(1, env_int("SPG_PULL_BLOCKS", 2));
+    const int pull_grid = std::max(1, ctx->num_sms * pull_per_sm / std::max(remote, 1));
+    base = 0;
     for (int s = 0; s < n; ++s) {
         const spg_csr* sl = slices[s];
         const int sd = sl->ctx->device;
@@ -774,6 +835,10 @@ spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n, cudaEvent_t 
             if (own) {
                 device_copy(ctx, st, out->colind + base, sl->colind, sl->nnz);
                 device_copy(ctx, st, out->values + base, sl->values, sl->nnz);
+            } else if (!pull_ce) {
+                k_pull_slice<<<pull_grid, 512, 0, st>>>(sl->colind, out->colind + base, sl->values, out->values + base,
+                                                        sl->nnz);
+                SPG_LAUNCH_CHECK();
             } else if (sd == dd) {
                 SPG_CUDA(cudaMemcpyAsync(out->colind + base, sl->colind, sl->nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
                 SPG_CUDA(cudaMemcpyAsync(out->values + base, sl->values, sl->nnz * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -785,22 +850,6 @@ spg_csr* vconcat(spg_ctx* ctx, const spg_csr* const* slices, int n, cudaEvent_t 
         if (log) SPG_CUDA(cudaEventRecord((*log)[s].t1, st));
         base += sl->nnz;
     }
-    // 2: the row pointers, rebased by kernels reading every slice's row
-    // pointers in place (peer access / IPC mapping: no staging copy)
-    int64_t r = 0;
-    base = 0;
-    for (int s = 0; s < n; ++s) {
-        const spg_csr* sl = slices[s];
-        if (sl->nrows) {
-            KTime kt(ctx, "vconcat_rebase");
-            k_rebase_rowptr<<<grid_for(ctx, sl->nrows), 256, 0, ctx->stream>>>(sl->rowptr, sl->nrows, base,
-                                                                                 out->rowptr + r + 1);
-            SPG_LAUNCH_CHECK();
-        }
-        r += sl->nrows;
-        base += sl->nnz;
-    }
-    if (rp_ready) SPG_CUDA(cudaEventRecord(rp_ready, ctx->stream));
     if (fork)
         for (int i = 0; i < std::min(n, spg_ctx::NAUX); ++i) {
             SPG_CUDA(cudaEventRecord(ctx->aux_ev[i], ctx->aux[i]));

@@ -159,3 +159,35 @@ def test_trident_tiles_on_distinct_devices(P, lam):
     assert np.array_equal(r.ledger, ref["ledger"])
     assert ours_multiset(r) == ref_multiset("trident", a, b, P, lam)
     assert r.xfer[:, 2].sum() > 0 and r.xfer[:, 0].sum() > 0
+
+
+@pytest.mark.skipif(spg.Device.count() < 2, reason="needs >= 2 GPUs (tiles on distinct devices, peer pulls)")
+@needs_ref
+@pytest.mark.parametrize("pull", ["1", "0"], ids=["copy_engines", "sm_pulls"])
+def test_peer_pull_modes_bit_exact(pull):
+    """vconcat's two ways of pulling a peer's B slice — copy engines
+    (cudaMemcpyPeerAsync) and the SM pull kernel (k_pull_slice, loads over
+    NVLink) — give the same C as the reference and the same ledger, with
+    slices whose destination offsets are not 16-byte aligned (odd nnz per
+    slice). The mode is read once per process, so the run is in a child."""
+    import subprocess
+    import sys
+    code = f"""
+import sys; sys.path.insert(0, {os.getcwd()!r})
+import numpy as np, oracle as O, paper_2603_21444_b200 as spg
+for P, lam, n in ((4, 4, 1999), (8, 2, 2001), (2, 2, 777)):
+    a, b = O.port_gen_erdos_renyi(n, 0.006, 31), O.port_gen_erdos_renyi(n, 0.006, 32)
+    r = spg.trident_spgemm(a, b, spg.TridentGrid.create(P, lam))
+    ref = O.ref_run_algo("trident", a, b, P, lam)
+    assert spg.pattern_equal(r.c, ref["c"]) and spg.allclose(r.c, ref["c"], 1e-12), (P, lam)
+    # a rank's rounds are one k-ordered multiply: bit-identical to the serial
+    # product (the reference's trident adds partial Cs at q = 2)
+    assert np.array_equal(np.asarray(r.c.values), np.asarray(O.port_spgemm(a, b).values)), (P, lam)
+    assert np.array_equal(r.ledger, ref["ledger"]), (P, lam)
+    assert r.xfer[:, 2].sum() > 0
+print("PULL_OK")
+"""
+    env = dict(os.environ, SPG_PULL_CE=pull)
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    assert "PULL_OK" in out.stdout

@@ -4,7 +4,10 @@ them, opens its peers' over NVLink and runs its rounds; rank 0 gathers the C
 tiles and reassembles C. C must equal the reference's spgemm_local product
 (csr.cpp:132-165) — bit-exact, since a rank's rounds run as one k-ordered
 multiply — for the N=2 grid (P, lambda) = (2, 2) and, on a 4-GPU box, the
-N=4 grid (4, 4) and the q=2 grid (4, 1). Skips with fewer GPUs than ranks."""
+N=4 grid (4, 4) and the q=2 grid (4, 1). Skips with fewer GPUs than ranks.
+Each grid runs with the peer slices pulled by the copy engines
+(SPG_PULL_CE=1) and by the SM pull kernel (SPG_PULL_CE=0); by default
+vconcat picks the SMs for >= 3 remote slices."""
 import os
 import socket
 import subprocess
@@ -61,13 +64,14 @@ def _port():
         return s.getsockname()[1]
 
 
+@pytest.mark.parametrize("pull", ["1", "0"], ids=["copy_engines", "sm_pulls"])
 @pytest.mark.parametrize("P,lam", [(2, 2), (4, 4), (4, 1)])
-def test_trident_rank_ipc_matches_reference(tmp_path, P, lam):
+def test_trident_rank_ipc_matches_reference(tmp_path, P, lam, pull):
     if spg.Device.count() < P:
         pytest.skip(f"needs {P} GPUs (one process per GPU)")
     import pickle
     out = str(tmp_path / "tiles.pkl")
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()))
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), SPG_PULL_CE=pull)
     code = WORKER.format(root=ROOT)
     procs = [subprocess.Popen([sys.executable, "-c", code, str(r), str(P), str(P), str(lam), out], env=env,
                               stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True) for r in range(P)]
