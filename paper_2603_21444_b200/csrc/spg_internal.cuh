@@ -66,7 +66,6 @@ struct spg_ctx {
     // Pinned host staging for small scalar read-backs.
     static constexpr int HOST_SCALAR_BYTES = 256;
     int64_t* host_scalars = nullptr;
-    bool tile_attr_set = false;
     // fork/join streams for concurrent slice copies (vconcat pulls from several peers at once)
     static constexpr int NAUX = 4;
     cudaStream_t aux[NAUX] = {};

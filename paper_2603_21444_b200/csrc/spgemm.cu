@@ -71,25 +71,11 @@ __device__ __forceinline__ int bucket_of(uint32_t col, int cshift, int nb) {
 }
 
 namespace tile {
-#ifndef SPG_TILE_NT
-#define SPG_TILE_NT 256
-#endif
-constexpr int NT = SPG_TILE_NT;                 // threads per CTA
+constexpr int NT = 256;                         // threads per CTA
 constexpr int NW = NT / 32;
 constexpr int SMALL_P = 512;                    // a tile row has <= SMALL_P products
 constexpr int SMALL_E = 64;                     // ... and <= SMALL_E entries
 constexpr int ROW_W_MAX = SMALL_P + 4 * SMALL_E + 4;
-#ifndef SPG_TILE_W
-#define SPG_TILE_W 2048
-#endif
-constexpr int TW = SPG_TILE_W;                  // tile window of the row weight prefix
-constexpr int PMAX = TW + ROW_W_MAX;            // bound of products, 4*entries, 4*rows of a tile
-constexpr int EMAX = PMAX / 4;
-constexpr int RMAX = PMAX / 4;
-constexpr int NJ = (PMAX + NT - 1) / NT;        // product slots per thread
-constexpr int EPT = (EMAX + NT - 1) / NT;       // entry slots per thread
-constexpr int HW = PMAX / 32 + 2;               // words of the head bitmap
-constexpr int LMAX = PMAX / 3 + 1;              // shared buckets of >= 3 products
 #ifndef SPG_TILE_BPP
 #define SPG_TILE_BPP 2
 #endif
@@ -101,6 +87,35 @@ constexpr int SP_BS = 30, SP_LEN = 30, SP_IN = 40, SP_PR = 52;
 constexpr int SP_LEN_MAX = 1023;
 constexpr uint64_t SP_BS_MASK = (uint64_t(1) << SP_BS) - 1;
 }  // namespace tile
+
+// Tile geometry: the window TW of the row weight prefix bounds a tile's
+// products, 4*entries and 4*rows by PMAX, which sizes the shared memory and
+// the per-thread product slots; MINB = CTAs per SM the registers are capped
+// for. Two are compiled (`profiles/r2o_*`, `r2u_*`): the wide one (84 KB, 2
+// CTAs/SM) is best when B's rows are short (config 2: 23.7 ms against 26.1),
+// the small one (3 CTAs/SM) when they are long (config 5, A*A^T with 64-entry
+// B rows: 34.6 ms against 38.5; a random B of that shape 26.1 against 27.8).
+#ifndef SPG_TILE_W
+#define SPG_TILE_W 2048
+#endif
+#ifndef SPG_TILE_MINB
+#define SPG_TILE_MINB 2
+#endif
+template <int TW_, int MINB_>
+struct TileGeo {
+    static constexpr int NT = tile::NT;
+    static constexpr int TW = TW_;
+    static constexpr int MINB = MINB_;
+    static constexpr int PMAX = TW + tile::ROW_W_MAX;     // bound of products, 4*entries, 4*rows of a tile
+    static constexpr int EMAX = PMAX / 4;
+    static constexpr int RMAX = PMAX / 4;
+    static constexpr int NJ = (PMAX + NT - 1) / NT;      // product slots per thread
+    static constexpr int EPT = (EMAX + NT - 1) / NT;     // entry slots per thread
+    static constexpr int HW = PMAX / 32 + 2;             // words of the head bitmap
+    static constexpr int LMAX = PMAX / 3 + 1;            // shared buckets of >= 3 products
+};
+using GeoWide = TileGeo<SPG_TILE_W, SPG_TILE_MINB>;
+using GeoSmall = TileGeo<1536, 3>;
 
 // Row kinds: SMALL rows share windowed tiles; a MEDIUM row (not small, but
 // products + 4*entries + 4 <= PMAX and every B row it reads <= SP_LEN_MAX
@@ -123,7 +138,7 @@ __host__ __device__ __forceinline__ bool tile_small(int64_t p, int64_t ne) {
 __global__ void k_row_prep(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
                            const int64_t* __restrict__ brp, int64_t m, int64_t* __restrict__ prod,
                            int64_t* __restrict__ wt, int8_t* __restrict__ kind, uint64_t* __restrict__ espan,
-                           int32_t* __restrict__ big_rows, int32_t* __restrict__ nbig, bool medium_big) {
+                           int32_t* __restrict__ big_rows, int32_t* __restrict__ nbig, bool medium_big, int pmax) {
     // half-warp per row (two rows in flight per warp: the row is a chain of
     // dependent loads arp -> acol -> brp); loops are warp-uniform
     const int lane = threadIdx.x & 31, sub = lane & 15, half = lane >> 4;
@@ -164,7 +179,7 @@ __global__ void k_row_prep(const int64_t* __restrict__ arp, const int32_t* __res
         for (int o = 8; o > 0; o >>= 1) maxlen = max(maxlen, static_cast<int64_t>(__shfl_xor_sync(FULL, maxlen, o)));
         int8_t rk = RK_BIG;
         if (tile_small(p, ne)) rk = RK_SMALL;
-        else if (!medium_big && tile_weight(p, ne) <= tile::PMAX && maxlen <= tile::SP_LEN_MAX) rk = RK_MEDIUM;
+        else if (!medium_big && tile_weight(p, ne) <= pmax && maxlen <= tile::SP_LEN_MAX) rk = RK_MEDIUM;
         const uint64_t pr = static_cast<uint64_t>(p);
         const bool spans = ok && rk != RK_BIG;
         {  // rows of <= 32 entries: in-row product offsets from registers
@@ -220,12 +235,12 @@ __global__ void k_row_prep(const int64_t* __restrict__ arp, const int32_t* __res
 
 // Tile starts: row i starts a tile if it is not SMALL, follows a row that is
 // not SMALL, or its weight prefix enters a new TW-window.
-__global__ void k_tile_flags(const int64_t* __restrict__ wpre, const int8_t* __restrict__ kind, int64_t m,
+__global__ void k_tile_flags(const int64_t* __restrict__ wpre, const int8_t* __restrict__ kind, int64_t m, int tw,
                              int64_t* __restrict__ flag) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
         int f = 1;
         if (i > 0 && kind[i] == RK_SMALL)
-            f = kind[i - 1] != RK_SMALL || (wpre[i] / tile::TW != wpre[i - 1] / tile::TW);
+            f = kind[i - 1] != RK_SMALL || (wpre[i] / tw != wpre[i - 1] / tw);
         flag[i] = f;
     }
 }
@@ -781,20 +796,21 @@ struct __align__(16) TileEnt {
     double av;     // A value
 };
 
+template <class G>
 struct __align__(16) TileSmem {
-    double val[tile::PMAX];        // staging: the tile's C entries (values)
-    TileEnt ent[tile::EMAX];
-    int32_t col[tile::PMAX];       // staging: columns
-    uint32_t cnt[tile::CW * tile::PMAX + 2];  // 2 x 16-bit bucket counters per word, then prefixes
-    uint32_t ebin[tile::EMAX];     // per entry: row bucket base (lo 16) | row bucket count (hi 16)
-    int32_t epre[tile::EMAX + 1];  // product prefix of the tile's entries
-    int32_t re[tile::RMAX + 1];    // first entry of each row (relative to the tile)
-    int32_t rend[tile::RMAX];      // end of each row in the (compacted) staging
-    uint32_t list[tile::LMAX];     // shared buckets of >= 3 products: start | end << 16
-    uint32_t dbm[tile::HW];        // duplicates: staged entries that repeat their predecessor's (row, column)
-    int32_t dpre[tile::HW];        //   and the word prefix of their count
-    uint16_t xs[tile::PMAX];       // product id of a staged entry of a shared bucket
-    uint16_t eof[tile::PMAX];      // entry of each product
+    double val[G::PMAX];        // staging: the tile's C entries (values)
+    TileEnt ent[G::EMAX];
+    int32_t col[G::PMAX];       // staging: columns
+    uint32_t cnt[tile::CW * G::PMAX + 2];  // 2 x 16-bit bucket counters per word, then prefixes
+    uint32_t ebin[G::EMAX];     // per entry: row bucket base (lo 16) | row bucket count (hi 16)
+    int32_t epre[G::EMAX + 1];  // product prefix of the tile's entries
+    int32_t re[G::RMAX + 1];    // first entry of each row (relative to the tile)
+    int32_t rend[G::RMAX];      // end of each row in the (compacted) staging
+    uint32_t list[G::LMAX];     // shared buckets of >= 3 products: start | end << 16
+    uint32_t dbm[G::HW];        // duplicates: staged entries that repeat their predecessor's (row, column)
+    int32_t dpre[G::HW];        //   and the word prefix of their count
+    uint16_t xs[G::PMAX];       // product id of a staged entry of a shared bucket
+    uint16_t eof[G::PMAX];      // entry of each product
     int32_t ws[4][tile::NW];       // scan workspaces (rotated)
     int64_t lbs[tile::NW];         // look-back: per-warp sums
     int32_t lbi[tile::NW];         //   and "found an inclusive prefix"
@@ -810,13 +826,15 @@ struct TileDesc {
 };
 
 // Number of duplicate entries before staging position q.
-__device__ __forceinline__ int dups_before(const TileSmem& S, int q) {
+template <class G>
+__device__ __forceinline__ int dups_before(const TileSmem<G>& S, int q) {
     return S.dpre[q >> 5] + __popc(S.dbm[q >> 5] & ((1u << (q & 31)) - 1u));
 }
 
 // Contiguous smem -> global copy of n staged entries to C[base, base+n) with
 // 16-byte stores in the aligned middle.
-__device__ __forceinline__ void tile_copy_out(const TileSmem& S, int n, int64_t base, int32_t* __restrict__ ccol,
+template <class G>
+__device__ __forceinline__ void tile_copy_out(const TileSmem<G>& S, int n, int64_t base, int32_t* __restrict__ ccol,
                                               double* __restrict__ cval, int tid) {
     {
         const int head = min(n, static_cast<int>((4 - (base & 3)) & 3));
@@ -869,11 +887,12 @@ __shared__ unsigned long long s_tp_last, s_tp_acc[16];
 // Prologue: the tile's rows and entries (contiguous in A and espan: one round
 // trip), the entry product prefix, the product -> entry map and the per-entry
 // row bucket ranges. Ends with the tables visible to the CTA.
-__device__ __forceinline__ TileDesc tile_prologue(TileSmem& S, int64_t k, const int64_t* __restrict__ arp,
+template <class G>
+__device__ __forceinline__ TileDesc tile_prologue(TileSmem<G>& S, int64_t k, const int64_t* __restrict__ arp,
                                                   const double* __restrict__ aval,
                                                   const uint64_t* __restrict__ espan,
                                                   const int64_t* __restrict__ tr, const int64_t* __restrict__ te) {
-    constexpr int NT = tile::NT, EPT = tile::EPT;
+    constexpr int NT = tile::NT, EPT = G::EPT;
     const int tid = threadIdx.x;
     TileDesc T;
     T.k = k;
@@ -929,8 +948,8 @@ __device__ __forceinline__ TileDesc tile_prologue(TileSmem& S, int64_t k, const 
 }
 
 // Gathers of the tile's products x = tid + NT*j (all issued, none consumed).
-template <int NJ>
-__device__ __forceinline__ void tile_gather(const TileSmem& S, int ptile, const int32_t* __restrict__ bcol,
+template <class G, int NJ>
+__device__ __forceinline__ void tile_gather(const TileSmem<G>& S, int ptile, const int32_t* __restrict__ bcol,
                                             const double* __restrict__ bval, int32_t (&col)[NJ], double (&val)[NJ],
                                             int (&aux)[NJ]) {
 #pragma unroll
@@ -940,7 +959,7 @@ __device__ __forceinline__ void tile_gather(const TileSmem& S, int ptile, const 
         const int x = threadIdx.x + tile::NT * j;
         if (x < ptile) {
             const int q = S.eof[x];
-            SPG_DCHECK(q >= 0 && q < tile::EMAX);
+            SPG_DCHECK(q >= 0 && q < G::EMAX);
             const int64_t u = S.ent[q].base + x;
             aux[j] = q;
             col[j] = __ldg(bcol + u);
@@ -951,8 +970,8 @@ __device__ __forceinline__ void tile_gather(const TileSmem& S, int ptile, const 
 
 // The tile's rows of C into the staging (sorted by (row, column), duplicates
 // combined in ascending k); S.rend[t] = end of row t. Returns the tile's nnz.
-template <int NJ>
-__device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int cshift, int32_t (&col)[NJ],
+template <class G, int NJ>
+__device__ __forceinline__ int tile_process(TileSmem<G>& S, const TileDesc& T, int cshift, int32_t (&col)[NJ],
                                             double (&val)[NJ], int (&aux)[NJ]) {
     constexpr int NT = tile::NT;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -985,7 +1004,7 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
         const int W = tile::CW * ptile;
         const int per = ((W + NT - 1) / NT) | 1;
         const int w0 = tid * per;
-        constexpr int PERMAX = ((tile::CW * tile::PMAX + NT - 1) / NT) | 1;
+        constexpr int PERMAX = ((tile::CW * G::PMAX + NT - 1) / NT) | 1;
         uint32_t wd[PERMAX];
         uint32_t s = 0;
 #pragma unroll
@@ -1038,7 +1057,7 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
             int b0 = 0;
             if (lane == 0) b0 = atomicAdd(&S.nlist, __popc(has));
             b0 = __shfl_sync(0xffffffffu, b0, 0);
-            SPG_DCHECK(!lreg || b0 + __popc(has & ((1u << lane) - 1u)) < tile::LMAX);
+            SPG_DCHECK(!lreg || b0 + __popc(has & ((1u << lane) - 1u)) < G::LMAX);
             if (lreg) S.list[b0 + __popc(has & ((1u << lane) - 1u))] = lreg;
         }
     }
@@ -1106,7 +1125,7 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
     // = ascending k.
     const int hw = (ptile >> 5) + 1;
     if (warp == 0) {
-        constexpr int PW = (tile::HW + 31) / 32;
+        constexpr int PW = (G::HW + 31) / 32;
         int c[PW], sum = 0;
 #pragma unroll
         for (int u = 0; u < PW; ++u) {
@@ -1118,7 +1137,7 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
 #pragma unroll
         for (int u = 0; u < PW; ++u) {
             const int w = lane * PW + u;
-            if (w < tile::HW) S.dpre[w] = pre;
+            if (w < G::HW) S.dpre[w] = pre;
             pre += c[u];
         }
     }
@@ -1157,7 +1176,8 @@ __device__ __forceinline__ int tile_process(TileSmem& S, const TileDesc& T, int 
 // predecessors per round trip). Tile k only waits on tiles with smaller
 // tickets, whose CTAs publish their aggregates without waiting on anything,
 // so the chain always makes progress.
-__device__ __forceinline__ int64_t tile_look_back(TileSmem& S, uint64_t* status, int64_t k, uint64_t s_first) {
+template <class G>
+__device__ __forceinline__ int64_t tile_look_back(TileSmem<G>& S, uint64_t* status, int64_t k, uint64_t s_first) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int64_t excl = 0;
     for (int64_t j0 = k - 1; j0 >= 0; j0 -= tile::NT) {
@@ -1191,23 +1211,21 @@ __device__ __forceinline__ int64_t tile_look_back(TileSmem& S, uint64_t* status,
     return excl;
 }
 
-#ifndef SPG_TILE_MINB
-#define SPG_TILE_MINB 2
-#endif
 // Persistent tile kernel. Per CTA, tiles come from a global ticket; for tile F
 // the order is: process F (its products already in registers) -> publish F's
 // aggregate -> prologue + gathers of the next tile -> look-back, row pointers
 // and copy-out of F (overlapping the next tile's gather latency).
-__global__ void __launch_bounds__(tile::NT, SPG_TILE_MINB) k_tile(
+template <class G>
+__global__ void __launch_bounds__(G::NT, G::MINB) k_tile(
     const int64_t* __restrict__ arp, const double* __restrict__ aval, const uint64_t* __restrict__ espan,
     const int32_t* __restrict__ bcol, const double* __restrict__ bval, const int64_t* __restrict__ tr,
     const int64_t* __restrict__ te, int64_t ntiles, unsigned long long* __restrict__ ticket, int cshift,
     const uint64_t* __restrict__ side_cp, const uint64_t* __restrict__ side_vp, const int64_t* __restrict__ side_nnz,
     uint64_t* __restrict__ status,
     int64_t* __restrict__ crp, int32_t* __restrict__ ccol, double* __restrict__ cval) {
-    constexpr int NT = tile::NT, NJ = tile::NJ;
+    constexpr int NT = tile::NT, NJ = G::NJ;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    TileSmem& S = *reinterpret_cast<TileSmem*>(smem_raw);
+    TileSmem<G>& S = *reinterpret_cast<TileSmem<G>*>(smem_raw);
     const int tid = threadIdx.x;
     TPROF_DECL
 
@@ -1219,7 +1237,7 @@ __global__ void __launch_bounds__(tile::NT, SPG_TILE_MINB) k_tile(
     double val[NJ];
     int aux[NJ];
     TileDesc T = tile_prologue(S, k0, arp, aval, espan, tr, te);
-    if (!T.big) tile_gather<NJ>(S, T.ptile, bcol, bval, col, val, aux);
+    if (!T.big) tile_gather<G, NJ>(S, T.ptile, bcol, bval, col, val, aux);
     while (true) {
 #ifdef SPG_TICKET_SMEM
         if (tid == 0) S.ticket = static_cast<int64_t>(atomicAdd(ticket, 1ull));
@@ -1230,7 +1248,7 @@ __global__ void __launch_bounds__(tile::NT, SPG_TILE_MINB) k_tile(
         if (tid == 0) tk = atomicAdd(ticket, 1ull);
 #endif
         TPROF(0)
-        const int nnz = T.big ? 0 : tile_process<NJ>(S, T, cshift, col, val, aux);
+        const int nnz = T.big ? 0 : tile_process<G, NJ>(S, T, cshift, col, val, aux);
         TPROF(1)
         const int64_t agg = T.big ? side_nnz[T.r0] : static_cast<int64_t>(nnz);
         if (tid == 0) st_status(status + T.k, (T.k == 0 ? ST_INC : ST_AGG) | static_cast<uint64_t>(agg));
@@ -1245,7 +1263,7 @@ __global__ void __launch_bounds__(tile::NT, SPG_TILE_MINB) k_tile(
         if (more) {
             T = tile_prologue(S, k2, arp, aval, espan, tr, te);
             TPROF(3)
-            if (!T.big) tile_gather<NJ>(S, T.ptile, bcol, bval, col, val, aux);
+            if (!T.big) tile_gather<G, NJ>(S, T.ptile, bcol, bval, col, val, aux);
             TPROF(4)
         }
         // finish F: offset, row pointers, copy-out
@@ -1581,11 +1599,42 @@ int cshift_for(int64_t ncols) {
     return 32 - bits;  // col << cshift puts the top column bit at bit 31
 }
 
+// The tile kernel of geometry G over the tiles [0, ntiles).
+template <class G>
+void launch_tiles(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const uint64_t* espan, const int64_t* tr,
+                  const int64_t* te, int64_t ntiles, unsigned long long* ticket, int cshift, const uint64_t* side_cp,
+                  const uint64_t* side_vp, const int64_t* side_nnz, uint64_t* status, spg_csr* c) {
+    static bool attr_set[64] = {};
+    if (ctx->device >= 64 || !attr_set[ctx->device]) {
+        SPG_CUDA(cudaFuncSetAttribute(k_tile<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem<G>)));
+        if (ctx->device < 64) attr_set[ctx->device] = true;
+    }
+    int occ = 1;
+    SPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile<G>, G::NT, sizeof(TileSmem<G>)));
+    const int grid = static_cast<int>(std::min<int64_t>(ntiles, int64_t(ctx->num_sms) * std::max(occ, 1)));
+    KTime kt(ctx, "spgemm_tile");
+    k_tile<G><<<grid, G::NT, sizeof(TileSmem<G>), ctx->stream>>>(a->rowptr, a->values, espan, b->colind, b->values, tr,
+                                                                 te, ntiles, ticket, cshift, side_cp, side_vp,
+                                                                 side_nnz, status, c->rowptr, c->colind, c->values);
+    SPG_LAUNCH_CHECK();
+}
+
+// Tile geometry by B's mean row length (known before any kernel): long B
+// rows (>= 32 entries) take the small tiles. SPG_TILE_GEO=wide|small forces one.
+bool small_tiles(const spg_csr* b) {
+    static const char* g = std::getenv("SPG_TILE_GEO");
+    if (g && g[0] == 'w') return false;
+    if (g && g[0] == 's') return true;
+    return b->nrows > 0 && b->nnz >= 32 * b->nrows;
+}
+
 // Single-pass tiled multiply.
 spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEvent_t b_data) {
     HostProf hprof;
     const int64_t m = a->nrows, n = b->ncols;
     const int cshift = cshift_for(n);
+    const bool small = small_tiles(b);
+    const int pmax = small ? GeoSmall::PMAX : GeoWide::PMAX, tw = small ? GeoSmall::TW : GeoWide::TW;
     // BIG rows (and, with the hub path, MEDIUM rows too: single-row tiles whose
     // cost varies 10x stall k_tile's look-back chain) go to the side path
     static const char* esc_env = std::getenv("SPG_BIG_ESC");
@@ -1599,7 +1648,7 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEven
     {
         KTime kt(ctx, "row_prep");
         k_row_prep<<<grid_for(ctx, 32 * m), 256, 0, ctx->stream>>>(a->rowptr, a->colind, b->rowptr, m, prod, wt,
-                                                                   kind, espan, big_list, nbig_d, hub);
+                                                                   kind, espan, big_list, nbig_d, hub, pmax);
         SPG_LAUNCH_CHECK();
     }
     {
@@ -1613,7 +1662,7 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEven
     exclusive_scan_i64(ctx, wt, wpre, m);
     {
         KTime kt(ctx, "tile_setup");
-        k_tile_flags<<<grid_for(ctx, m), 256, 0, ctx->stream>>>(wpre, kind, m, flag);
+        k_tile_flags<<<grid_for(ctx, m), 256, 0, ctx->stream>>>(wpre, kind, m, tw, flag);
         SPG_LAUNCH_CHECK();
     }
     exclusive_scan_i64(ctx, flag, fpos, m);
@@ -1662,20 +1711,10 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEven
     spg_csr* c = new_csr(ctx, m, n, -1);
     alloc_c_arrays(ctx, c, products - big_products + big_nnz);  // upper bound of nnz(C)
     SPG_CUDA(cudaMemsetAsync(c->rowptr, 0, sizeof(int64_t), ctx->stream));
-    if (!ctx->tile_attr_set) {
-        SPG_CUDA(cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem)));
-        ctx->tile_attr_set = true;
-    }
-    int occ = 1;
-    SPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile, tile::NT, sizeof(TileSmem)));
-    const int grid = static_cast<int>(std::min<int64_t>(ntiles, int64_t(ctx->num_sms) * std::max(occ, 1)));
-    {
-        KTime kt(ctx, "spgemm_tile");
-        k_tile<<<grid, tile::NT, sizeof(TileSmem), ctx->stream>>>(a->rowptr, a->values, espan, b->colind, b->values,
-                                                                  tr, te, ntiles, ticket, cshift, side_cp, side_vp,
-                                                                  side_nnz, status, c->rowptr, c->colind, c->values);
-        SPG_LAUNCH_CHECK();
-    }
+    if (small)
+        launch_tiles<GeoSmall>(ctx, a, b, espan, tr, te, ntiles, ticket, cshift, side_cp, side_vp, side_nnz, status, c);
+    else
+        launch_tiles<GeoWide>(ctx, a, b, espan, tr, te, ntiles, ticket, cshift, side_cp, side_vp, side_nnz, status, c);
     if (nbig && hub) {
         hub_numeric(ctx, a, b, drows, nbig, gbm, c);
     } else if (nbig) {

@@ -1,4 +1,6 @@
-"""Per-kernel times of config 5 (k-mer A*A^T), or config 2 with argument `er` (dev tool)."""
+"""Per-kernel times of config 5 (k-mer A*A^T), or config 2 with argument `er`, or
+`rand`: config 5's shapes with a random B (2^18 x 2^22, 64/row: long B rows like
+A^T's, but no structural duplicates) (dev tool)."""
 import sys
 import time
 sys.path.insert(0, ".")
@@ -7,6 +9,9 @@ import paper_2603_21444_b200 as spg  # noqa: E402
 if len(sys.argv) > 1 and sys.argv[1] == "er":  # config 2 instead
     a = spg.gen_erdos_renyi(1 << 22, 16.0 / (1 << 22), 1)
     at = a
+elif len(sys.argv) > 1 and sys.argv[1] == "rand":
+    a = spg.gen_erdos_renyi_rect(1 << 22, 1 << 18, 2.0 ** -16, 5)
+    at = spg.gen_erdos_renyi_rect(1 << 18, 1 << 22, 2.0 ** -16, 6)
 else:
     a = spg.gen_erdos_renyi_rect(1 << 22, 1 << 18, 2.0 ** -16, 5)
     at = spg.transpose(a)
@@ -24,7 +29,7 @@ for _ in range(3):
     nnz = c.nnz
     del c
 dev.synchronize()
-print(f"config5 wall/step {1e3 * (time.perf_counter() - t0) / 3:.2f} ms nnz {nnz}")
+print(f"{sys.argv[1] if len(sys.argv) > 1 else 'config5'} wall/step {1e3 * (time.perf_counter() - t0) / 3:.2f} ms nnz {nnz}")
 for k, (n, ms) in sorted(dev.timing_read().items()):
     print(f"   {k:20s} {ms / max(n, 1):10.3f} ms x{n}")
 

@@ -374,3 +374,47 @@ np.save(%r, np.concatenate([np.asarray(c.rowptr, np.float64), np.asarray(c.colin
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(f))
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_tile_geometries_bit_exact():
+    """Both compiled tile geometries (wide: 2048 window, 2 CTAs/SM; small:
+    1536 window, 3 CTAs/SM — picked by B's mean row length) give the
+    oracle's C bit-exact on short-row B, long-row B, A*A^T (a duplicate in
+    every row) and MEDIUM rows that fit one geometry's tiles but not the
+    other's. SPG_TILE_GEO is read once per process: one child per geometry."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = f"""
+import sys; sys.path.insert(0, {root!r})
+import numpy as np, oracle as O, paper_2603_21444_b200 as spg
+d = spg.Device(0)
+def same(a, b):
+    return (np.array_equal(a.rowptr, b.rowptr) and np.array_equal(np.asarray(a.colind, np.int64),
+            np.asarray(b.colind, np.int64)) and np.array_equal(a.values, b.values))
+cases = []
+a = O.port_gen_erdos_renyi(3000, 0.005, 41); cases.append((a, a))                      # short B rows
+a = O.port_gen_erdos_renyi_rect(6000, 600, 4 / 600, 42)
+cases.append((a, O.port_gen_erdos_renyi_rect(600, 6000, 64 / 6000, 43)))                # long B rows
+import scipy.sparse as sp
+t = sp.csr_matrix((a.values, a.colind, a.rowptr), shape=(a.nrows, a.ncols)).T.tocsr()
+t.sort_indices()
+cases.append((a, O.Csr(a.ncols, a.nrows, t.indptr.astype(np.int64), t.indices.astype(np.int32),
+                       t.data.astype(np.float64))))                                     # A*A^T
+# rows of 1200-3700 products (weights around both geometries' PMAX, 2308 and
+# 2820) over a B wider than the hub takes: MEDIUM tiles in one geometry are
+# BIG (ESC) rows in the other
+a = O.port_gen_erdos_renyi_rect(400, 4000, 40 / 4000, 44)
+cases.append((a, O.port_gen_erdos_renyi_rect(4000, 300000, 60 / 300000, 45)))
+for i, (a, b) in enumerate(cases):
+    c = d.spgemm(d.upload(a), d.upload(b))
+    c.check()
+    assert same(c.download(), O.port_spgemm(a, b)), i
+print("GEO_OK")
+"""
+    for geo in ("wide", "small"):
+        env = dict(os.environ, SPG_TILE_GEO=geo)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, (geo, r.stderr[-2000:])
+        assert "GEO_OK" in r.stdout
