@@ -602,6 +602,7 @@ __global__ void k_peek(const unsigned char* __restrict__ src, unsigned char* __r
 void* peek_async(spg_ctx* ctx, int off, const void* dsrc, int bytes) {
     if (off < 0 || off + bytes > spg_ctx::HOST_SCALAR_BYTES) fail(SPG_ERROR, "peek_async: slot out of range");
     unsigned char* dst = reinterpret_cast<unsigned char*>(ctx->host_scalars) + off;
+    KTime kt(ctx, "peek");
     k_peek<<<1, 32, 0, ctx->stream>>>(static_cast<const unsigned char*>(dsrc), dst, bytes);
     SPG_LAUNCH_CHECK();
     return dst;

@@ -1619,13 +1619,42 @@ void launch_tiles(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const uint64
     SPG_LAUNCH_CHECK();
 }
 
-// Tile geometry by B's mean row length (known before any kernel): long B
-// rows (>= 32 entries) take the small tiles. SPG_TILE_GEO=wide|small forces one.
-bool small_tiles(const spg_csr* b) {
+// Sum of the lengths of the B rows referenced by n evenly spaced entries of A.
+__global__ void k_ref_len(const int32_t* __restrict__ acol, int64_t stride, int64_t n,
+                          const int64_t* __restrict__ brp, unsigned long long* __restrict__ out) {
+    unsigned long long s = 0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const int32_t k = __ldg(acol + i * stride);
+        s += static_cast<unsigned long long>(__ldg(brp + k + 1) - __ldg(brp + k));
+    }
+    s = warp_reduce_sum(s);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
+// Tile geometry by the mean length of the B rows that A's entries reference
+// (= products / nnz(A)), estimated from up to 65536 evenly spaced entries
+// before the row pass (A with >= 2^20 entries): >= 32 takes the small tiles
+// (config 5: 64, R-MAT: 744 — its tile rows gather from hub rows; configs 2
+// and 4: 16, config 1: 8).
+// One read-back through the mapped scalars. SPG_TILE_GEO=wide|small forces one.
+bool small_tiles(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
     static const char* g = std::getenv("SPG_TILE_GEO");
     if (g && g[0] == 'w') return false;
     if (g && g[0] == 's') return true;
-    return b->nrows > 0 && b->nnz >= 32 * b->nrows;
+    // small multiplies: the read-back would cost more than the geometry gains
+    // (config 1, 1.3e5 entries: 0.157 -> 0.175 ms with it)
+    if (a->nnz < (int64_t(1) << 20) || b->nrows == 0) return false;
+    const int64_t n = std::min<int64_t>(a->nnz, 65536), stride = a->nnz / n;
+    DBuf<unsigned long long> sum(ctx, 1);
+    SPG_CUDA(cudaMemsetAsync(sum.get(), 0, sizeof(unsigned long long), ctx->stream));
+    KTime kt(ctx, "tile_geometry");
+    k_ref_len<<<static_cast<int>(std::min<int64_t>((n + 255) / 256, 256)), 256, 0, ctx->stream>>>(a->colind, stride, n,
+                                                                                               b->rowptr, sum);
+    SPG_LAUNCH_CHECK();
+    const volatile unsigned long long* h =
+        static_cast<unsigned long long*>(peek_async(ctx, 88, sum.get(), sizeof(unsigned long long)));
+    SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return *h >= 32ull * static_cast<unsigned long long>(n);
 }
 
 // Single-pass tiled multiply.
@@ -1633,7 +1662,7 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEven
     HostProf hprof;
     const int64_t m = a->nrows, n = b->ncols;
     const int cshift = cshift_for(n);
-    const bool small = small_tiles(b);
+    const bool small = small_tiles(ctx, a, b);
     const int pmax = small ? GeoSmall::PMAX : GeoWide::PMAX, tw = small ? GeoSmall::TW : GeoWide::TW;
     // BIG rows (and, with the hub path, MEDIUM rows too: single-row tiles whose
     // cost varies 10x stall k_tile's look-back chain) go to the side path
