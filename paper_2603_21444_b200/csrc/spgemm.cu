@@ -117,6 +117,16 @@ struct TileGeo {
 using GeoWide = TileGeo<SPG_TILE_W, SPG_TILE_MINB>;
 using GeoSmall = TileGeo<1536, 3>;
 
+// The geometry decision, made identically by the row pass, the tile flags
+// (on the device, from the sampled sum, so no host round trip precedes the
+// row pass) and the host (after its one read-back): force 1 = wide, 2 =
+// small, else small iff the nsamp sampled entries of A reference B rows of
+// mean length >= 32.
+__host__ __device__ __forceinline__ bool geo_small(unsigned long long refsum, int64_t nsamp, int force) {
+    if (force) return force == 2;
+    return nsamp > 0 && refsum >= 32ull * static_cast<unsigned long long>(nsamp);
+}
+
 // Row kinds: SMALL rows share windowed tiles; a MEDIUM row (not small, but
 // products + 4*entries + 4 <= PMAX and every B row it reads <= SP_LEN_MAX
 // long) is a tile of its own; BIG rows go to the side path.
@@ -138,7 +148,9 @@ __host__ __device__ __forceinline__ bool tile_small(int64_t p, int64_t ne) {
 __global__ void k_row_prep(const int64_t* __restrict__ arp, const int32_t* __restrict__ acol,
                            const int64_t* __restrict__ brp, int64_t m, int64_t* __restrict__ prod,
                            int64_t* __restrict__ wt, int8_t* __restrict__ kind, uint64_t* __restrict__ espan,
-                           int32_t* __restrict__ big_rows, int32_t* __restrict__ nbig, bool medium_big, int pmax) {
+                           int32_t* __restrict__ big_rows, int32_t* __restrict__ nbig, bool medium_big,
+                           const unsigned long long* __restrict__ refsum, int64_t nsamp, int force) {
+    const int pmax = geo_small(*refsum, nsamp, force) ? GeoSmall::PMAX : GeoWide::PMAX;
     // half-warp per row (two rows in flight per warp: the row is a chain of
     // dependent loads arp -> acol -> brp); loops are warp-uniform
     const int lane = threadIdx.x & 31, sub = lane & 15, half = lane >> 4;
@@ -235,8 +247,10 @@ __global__ void k_row_prep(const int64_t* __restrict__ arp, const int32_t* __res
 
 // Tile starts: row i starts a tile if it is not SMALL, follows a row that is
 // not SMALL, or its weight prefix enters a new TW-window.
-__global__ void k_tile_flags(const int64_t* __restrict__ wpre, const int8_t* __restrict__ kind, int64_t m, int tw,
+__global__ void k_tile_flags(const int64_t* __restrict__ wpre, const int8_t* __restrict__ kind, int64_t m,
+                             const unsigned long long* __restrict__ refsum, int64_t nsamp, int force,
                              int64_t* __restrict__ flag) {
+    const int64_t tw = geo_small(*refsum, nsamp, force) ? GeoSmall::TW : GeoWide::TW;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
         int f = 1;
         if (i > 0 && kind[i] == RK_SMALL)
@@ -1632,29 +1646,25 @@ __global__ void k_ref_len(const int32_t* __restrict__ acol, int64_t stride, int6
 }
 
 // Tile geometry by the mean length of the B rows that A's entries reference
-// (= products / nnz(A)), estimated from up to 65536 evenly spaced entries
-// before the row pass (A with >= 2^20 entries): >= 32 takes the small tiles
-// (config 5: 64, R-MAT: 744 — its tile rows gather from hub rows; configs 2
-// and 4: 16, config 1: 8).
-// One read-back through the mapped scalars. SPG_TILE_GEO=wide|small forces one.
-bool small_tiles(spg_ctx* ctx, const spg_csr* a, const spg_csr* b) {
+// (= products / nnz(A)), estimated from up to 65536 evenly spaced entries of
+// A (when A has >= 2^20 entries; smaller multiplies take the wide tiles):
+// >= 32 takes the small tiles (config 5: 64, R-MAT: 744 — its tile rows
+// gather from hub rows; configs 2 and 4: 16, config 1: 8). The sum stays on
+// the device for the row pass and the tile flags; the host reads it with the
+// row pass's totals. SPG_TILE_GEO=wide|small forces one.
+int tile_geo_force() {
     static const char* g = std::getenv("SPG_TILE_GEO");
-    if (g && g[0] == 'w') return false;
-    if (g && g[0] == 's') return true;
-    // small multiplies: the read-back would cost more than the geometry gains
-    // (config 1, 1.3e5 entries: 0.157 -> 0.175 ms with it)
-    if (a->nnz < (int64_t(1) << 20) || b->nrows == 0) return false;
+    return (g && g[0] == 'w') ? 1 : (g && g[0] == 's') ? 2 : 0;
+}
+int64_t sample_ref_len(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, unsigned long long* refsum) {
+    SPG_CUDA(cudaMemsetAsync(refsum, 0, sizeof(unsigned long long), ctx->stream));
+    if (tile_geo_force() || a->nnz < (int64_t(1) << 20) || b->nrows == 0) return 0;
     const int64_t n = std::min<int64_t>(a->nnz, 65536), stride = a->nnz / n;
-    DBuf<unsigned long long> sum(ctx, 1);
-    SPG_CUDA(cudaMemsetAsync(sum.get(), 0, sizeof(unsigned long long), ctx->stream));
     KTime kt(ctx, "tile_geometry");
     k_ref_len<<<static_cast<int>(std::min<int64_t>((n + 255) / 256, 256)), 256, 0, ctx->stream>>>(a->colind, stride, n,
-                                                                                               b->rowptr, sum);
+                                                                                               b->rowptr, refsum);
     SPG_LAUNCH_CHECK();
-    const volatile unsigned long long* h =
-        static_cast<unsigned long long*>(peek_async(ctx, 88, sum.get(), sizeof(unsigned long long)));
-    SPG_CUDA(cudaStreamSynchronize(ctx->stream));
-    return *h >= 32ull * static_cast<unsigned long long>(n);
+    return n;
 }
 
 // Single-pass tiled multiply.
@@ -1662,8 +1672,9 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEven
     HostProf hprof;
     const int64_t m = a->nrows, n = b->ncols;
     const int cshift = cshift_for(n);
-    const bool small = small_tiles(ctx, a, b);
-    const int pmax = small ? GeoSmall::PMAX : GeoWide::PMAX, tw = small ? GeoSmall::TW : GeoWide::TW;
+    const int force = tile_geo_force();
+    DBuf<unsigned long long> refsum(ctx, 1);
+    const int64_t nsamp = sample_ref_len(ctx, a, b, refsum);
     // BIG rows (and, with the hub path, MEDIUM rows too: single-row tiles whose
     // cost varies 10x stall k_tile's look-back chain) go to the side path
     static const char* esc_env = std::getenv("SPG_BIG_ESC");
@@ -1677,7 +1688,8 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEven
     {
         KTime kt(ctx, "row_prep");
         k_row_prep<<<grid_for(ctx, 32 * m), 256, 0, ctx->stream>>>(a->rowptr, a->colind, b->rowptr, m, prod, wt,
-                                                                   kind, espan, big_list, nbig_d, hub, pmax);
+                                                                   kind, espan, big_list, nbig_d, hub, refsum,
+                                                                   nsamp, force);
         SPG_LAUNCH_CHECK();
     }
     {
@@ -1691,18 +1703,21 @@ spg_csr* spgemm_tiled(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, cudaEven
     exclusive_scan_i64(ctx, wt, wpre, m);
     {
         KTime kt(ctx, "tile_setup");
-        k_tile_flags<<<grid_for(ctx, m), 256, 0, ctx->stream>>>(wpre, kind, m, tw, flag);
+        k_tile_flags<<<grid_for(ctx, m), 256, 0, ctx->stream>>>(wpre, kind, m, refsum, nsamp, force, flag);
         SPG_LAUNCH_CHECK();
     }
     exclusive_scan_i64(ctx, flag, fpos, m);
     const volatile int32_t* hnbig = static_cast<int32_t*>(peek_async(ctx, 64, nbig_d.get(), sizeof(int32_t)));
     const volatile int64_t* hprod = static_cast<int64_t*>(peek_async(ctx, 72, total.get(), sizeof(int64_t)));
     const volatile int64_t* hnt = static_cast<int64_t*>(peek_async(ctx, 80, fpos.get() + m, sizeof(int64_t)));
+    const volatile unsigned long long* hrs =
+        static_cast<unsigned long long*>(peek_async(ctx, 88, refsum.get(), sizeof(unsigned long long)));
     hprof.mark("launch1");
     SPG_CUDA(cudaStreamSynchronize(ctx->stream));
     hprof.mark("sync1");
     const int nbig = *hnbig;
     const int64_t products = *hprod, ntiles = *hnt;
+    const bool small = geo_small(*hrs, nsamp, force);  // the decision the row pass and the flags made
     // B's columns and values may still be arriving (trident pulls): everything
     // above read only B's row pointers
     if (b_data) SPG_CUDA(cudaStreamWaitEvent(ctx->stream, b_data, 0));
