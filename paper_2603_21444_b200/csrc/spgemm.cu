@@ -519,8 +519,9 @@ __global__ void k_big_finish(const int32_t* __restrict__ rows, int nrows, const 
 // ------------------------------------------- BIG rows: dense hub accumulator
 // Rows too large for a tile (R-MAT hubs: up to 3.6e7 products) without a
 // sort, for B with at most HUB_W columns. One CTA per row (rows from a
-// ticket, heaviest first); warp w owns the column range [w*HUB_RANGE,
-// (w+1)*HUB_RANGE) with a shared-memory bitmap of its columns.
+// ticket, heaviest first); warp w owns the column range [w*RANGE,
+// (w+1)*RANGE) of the 2^18-column window with a shared-memory bitmap of its
+// columns (RANGE = 16384 in the symbolic pass, 8192 in the numeric pass).
 //  * symbolic (k_hub_sym): every warp walks the row's entries — 32 lanes
 //    binary-search 32 entries' B rows for the warp's range at once, then set
 //    the bits of the entries' columns — and stores its bitmap; the row's nnz
@@ -534,19 +535,33 @@ __global__ void k_big_finish(const int32_t* __restrict__ rows, int nrows, const 
 //    then + a*b in ascending k, accumulated in place in C: bit-identical to the
 //    reference's acc[j] += av*bv. The running sums live in the row's own C
 //    range (compact, L2-resident), not in a dense scratch.
-constexpr int HUB_NW = 8, HUB_RANGE = 32768, HUB_W = HUB_NW * HUB_RANGE, HUB_WORDS = HUB_RANGE / 32;
-constexpr int HUB_ACC = 1536;  // running sums a warp keeps in shared memory
+// Warps per CTA: the symbolic pass 16 (ranges of 16384 columns), the numeric
+// pass 32 (8192): the numeric pass waits a DRAM round trip per entry and warp,
+// and its shared memory allows one CTA per SM, so more warps over narrower
+// ranges hide more latency (R-MAT 18: numeric 67.2 ms with 8 warps, 56.5 with
+// 16, 51.8 with 32; symbolic 7.9 / 6.5 / 9.6; `profiles/r2y_hub_warps.txt`).
+// Both address a row's bitmap in column order, so their splits are independent.
+#ifndef SPG_HUB_SYM_NW
+#define SPG_HUB_SYM_NW 16
+#endif
+#ifndef SPG_HUB_NUM_NW
+#define SPG_HUB_NUM_NW 32
+#endif
+constexpr int HUB_W = 262144;  // columns of one hub window (2^18)
+constexpr int SYM_NW = SPG_HUB_SYM_NW, SYM_RANGE = HUB_W / SYM_NW, SYM_WORDS = SYM_RANGE / 32;
+constexpr int NUM_NW = SPG_HUB_NUM_NW, NUM_RANGE = HUB_W / NUM_NW, NUM_WORDS = NUM_RANGE / 32;
+constexpr int HUB_ACC = 12288 / NUM_NW;  // running sums a warp keeps in shared memory
 struct HubSymSmem {
-    uint32_t bm[HUB_NW][HUB_WORDS];  // the row's columns
-    int64_t cnt[HUB_NW];
+    uint32_t bm[SYM_NW][SYM_WORDS];  // the row's columns
+    int64_t cnt[SYM_NW];
     int row;
 };
 struct HubSmem {
-    double acc[HUB_NW][HUB_ACC];     // running sums at their rank (warps with <= HUB_ACC columns)
-    uint32_t sb[HUB_NW][HUB_WORDS];  // the row's columns (symbolic bitmap)
-    uint32_t sp[HUB_NW][HUB_WORDS];  // exclusive prefix of the words' popcounts
-    uint32_t bm[HUB_NW][HUB_WORDS];  // touched so far
-    int64_t cnt[HUB_NW];
+    double acc[NUM_NW][HUB_ACC];     // running sums at their rank (warps with <= HUB_ACC columns)
+    uint32_t sb[NUM_NW][NUM_WORDS];  // the row's columns (symbolic bitmap)
+    uint32_t sp[NUM_NW][NUM_WORDS];  // exclusive prefix of the words' popcounts
+    uint32_t bm[NUM_NW][NUM_WORDS];  // touched so far
+    int64_t cnt[NUM_NW];
     int row;
 };
 
@@ -577,7 +592,7 @@ __device__ __forceinline__ void hub_span(const int32_t* __restrict__ acol, const
     if (want_av) av = __ldg(aval + e);
 }
 
-__global__ void __launch_bounds__(32 * HUB_NW) k_hub_sym(const int32_t* __restrict__ rows, int nrows,
+__global__ void __launch_bounds__(32 * SYM_NW) k_hub_sym(const int32_t* __restrict__ rows, int nrows,
                                                          const int64_t* __restrict__ arp,
                                                          const int32_t* __restrict__ acol,
                                                          const int64_t* __restrict__ brp,
@@ -587,7 +602,7 @@ __global__ void __launch_bounds__(32 * HUB_NW) k_hub_sym(const int32_t* __restri
     HubSymSmem& S = *reinterpret_cast<HubSymSmem*>(hub_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t* my = S.bm[warp];
-    const int64_t lo_c = int64_t(warp) * HUB_RANGE, hi_c = lo_c + HUB_RANGE;
+    const int64_t lo_c = int64_t(warp) * SYM_RANGE, hi_c = lo_c + SYM_RANGE;
     while (true) {
         if (threadIdx.x == 0) S.row = static_cast<int>(atomicAdd(ticket, 1u));
         __syncthreads();
@@ -596,7 +611,7 @@ __global__ void __launch_bounds__(32 * HUB_NW) k_hub_sym(const int32_t* __restri
         if (t >= nrows) break;
         const int64_t i = rows[t];
         const int64_t e0 = arp[i], e1 = arp[i + 1];
-        for (int x = lane; x < HUB_WORDS; x += 32) my[x] = 0u;
+        for (int x = lane; x < SYM_WORDS; x += 32) my[x] = 0u;
         __syncwarp();
         for (int64_t c0 = e0; c0 < e1; c0 += 32) {
             int64_t s, f;
@@ -613,8 +628,8 @@ __global__ void __launch_bounds__(32 * HUB_NW) k_hub_sym(const int32_t* __restri
         }
         __syncwarp();
         int64_t cnt = 0;
-        uint32_t* g = gbm + static_cast<size_t>(t) * (HUB_W / 32) + static_cast<size_t>(warp) * HUB_WORDS;
-        for (int x = lane; x < HUB_WORDS; x += 32) {
+        uint32_t* g = gbm + static_cast<size_t>(t) * (HUB_W / 32) + static_cast<size_t>(warp) * SYM_WORDS;
+        for (int x = lane; x < SYM_WORDS; x += 32) {
             const uint32_t w = my[x];
             g[x] = w;
             cnt += __popc(w);
@@ -624,13 +639,13 @@ __global__ void __launch_bounds__(32 * HUB_NW) k_hub_sym(const int32_t* __restri
         __syncthreads();
         if (threadIdx.x == 0) {
             int64_t tot = 0;
-            for (int w = 0; w < HUB_NW; ++w) tot += S.cnt[w];
+            for (int w = 0; w < SYM_NW; ++w) tot += S.cnt[w];
             side_nnz[i] = tot;
         }
     }
 }
 
-__global__ void __launch_bounds__(32 * HUB_NW) k_hub_num(const int32_t* __restrict__ rows, int nrows,
+__global__ void __launch_bounds__(32 * NUM_NW) k_hub_num(const int32_t* __restrict__ rows, int nrows,
                                                          const int64_t* __restrict__ arp,
                                                          const int32_t* __restrict__ acol,
                                                          const double* __restrict__ aval,
@@ -646,8 +661,8 @@ __global__ void __launch_bounds__(32 * HUB_NW) k_hub_num(const int32_t* __restri
     uint32_t* sb = S.sb[warp];
     uint32_t* sp = S.sp[warp];
     uint32_t* bm = S.bm[warp];
-    const int64_t lo_c = int64_t(warp) * HUB_RANGE, hi_c = lo_c + HUB_RANGE;
-    constexpr int WPL = HUB_WORDS / 32;  // words per lane (contiguous)
+    const int64_t lo_c = int64_t(warp) * NUM_RANGE, hi_c = lo_c + NUM_RANGE;
+    constexpr int WPL = NUM_WORDS / 32;  // words per lane (contiguous)
     while (true) {
         if (threadIdx.x == 0) S.row = static_cast<int>(atomicAdd(ticket, 1u));
         __syncthreads();
@@ -657,7 +672,7 @@ __global__ void __launch_bounds__(32 * HUB_NW) k_hub_num(const int32_t* __restri
         const int64_t i = rows[t];
         const int64_t e0 = arp[i], e1 = arp[i + 1];
         // this warp's bitmap, the prefix of its popcounts, and its first C entry
-        const uint32_t* g = gbm + static_cast<size_t>(t) * (HUB_W / 32) + static_cast<size_t>(warp) * HUB_WORDS;
+        const uint32_t* g = gbm + static_cast<size_t>(t) * (HUB_W / 32) + static_cast<size_t>(warp) * NUM_WORDS;
         uint32_t wsum = 0;
 #pragma unroll 8
         for (int u = 0; u < WPL; ++u) {
@@ -1379,12 +1394,12 @@ struct HostProf {
 // symbolic pass sizes the rows (side_nnz) for k_tile; the numeric pass runs
 // after k_tile (hub_numeric). drows receives the BIG rows in ascending order.
 constexpr int64_t HUB_MAX_COLS = HUB_W;
-// CTAs per SM: the symbolic pass hides its latency with 2; the numeric pass
-// keeps the running sums of the rows in flight in L2, and one row per SM
-// measured best (R-MAT 18: 65.0 ms against 69.7 with 2)
+// CTAs per SM: the symbolic pass as many as fit (4 of 512 threads); the
+// numeric pass one (its shared memory; with 8 warps a second CTA was slower
+// too, R-MAT 18: 65.0 ms against 69.7 — the rows' running sums stay in L2)
 int hub_grid(spg_ctx* ctx, bool numeric) {
     static const char* g = std::getenv("SPG_HUB_CTAS");
-    return ctx->num_sms * (g ? std::atoi(g) : (numeric ? 1 : 6));
+    return ctx->num_sms * (g ? std::atoi(g) : (numeric ? 1 : 2048 / (32 * SYM_NW)));
 }
 void hub_attr(spg_ctx* ctx) {
     static bool done[64] = {};
@@ -1414,7 +1429,7 @@ int64_t hub_symbolic(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const int
     SPG_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), ctx->stream));
     {
         KTime kt(ctx, "hub_symbolic");
-        k_hub_sym<<<hub_grid(ctx, false), 32 * HUB_NW, sizeof(HubSymSmem), ctx->stream>>>(drows, nbig, a->rowptr, a->colind,
+        k_hub_sym<<<hub_grid(ctx, false), 32 * SYM_NW, sizeof(HubSymSmem), ctx->stream>>>(drows, nbig, a->rowptr, a->colind,
                                                                                b->rowptr, b->colind, ticket, gbm,
                                                                                side_nnz);
         SPG_LAUNCH_CHECK();
@@ -1440,7 +1455,7 @@ void hub_numeric(spg_ctx* ctx, const spg_csr* a, const spg_csr* b, const int32_t
     DBuf<unsigned> ticket(ctx, 1);
     SPG_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), ctx->stream));
     KTime kt(ctx, "hub_numeric");
-    k_hub_num<<<hub_grid(ctx, true), 32 * HUB_NW, sizeof(HubSmem), ctx->stream>>>(
+    k_hub_num<<<hub_grid(ctx, true), 32 * NUM_NW, sizeof(HubSmem), ctx->stream>>>(
         drows, nbig, a->rowptr, a->colind, a->values, b->rowptr, b->colind, b->values, ticket, gbm, c->rowptr,
         c->colind, c->values);
     SPG_LAUNCH_CHECK();
