@@ -550,14 +550,12 @@ __global__ void k_big_finish(const int32_t* __restrict__ rows, int nrows, const 
 constexpr int HUB_W = 262144;  // columns of one hub window (2^18)
 constexpr int SYM_NW = SPG_HUB_SYM_NW, SYM_RANGE = HUB_W / SYM_NW, SYM_WORDS = SYM_RANGE / 32;
 constexpr int NUM_NW = SPG_HUB_NUM_NW, NUM_RANGE = HUB_W / NUM_NW, NUM_WORDS = NUM_RANGE / 32;
-constexpr int HUB_ACC = 12288 / NUM_NW;  // running sums a warp keeps in shared memory
 struct HubSymSmem {
     uint32_t bm[SYM_NW][SYM_WORDS];  // the row's columns
     int64_t cnt[SYM_NW];
     int row;
 };
 struct HubSmem {
-    double acc[NUM_NW][HUB_ACC];     // running sums at their rank (warps with <= HUB_ACC columns)
     uint32_t sb[NUM_NW][NUM_WORDS];  // the row's columns (symbolic bitmap)
     uint32_t sp[NUM_NW][NUM_WORDS];  // exclusive prefix of the words' popcounts
     uint32_t bm[NUM_NW][NUM_WORDS];  // touched so far
@@ -695,11 +693,10 @@ __global__ void __launch_bounds__(32 * NUM_NW) k_hub_num(const int32_t* __restri
         for (int w = 0; w < warp; ++w) base += S.cnt[w];
         int32_t* oc = ccol + base;
         double* ov = cval + base;
-        // the running sums: in shared memory when the warp's columns fit, else
-        // in place in C (L2)
-        const uint32_t nw = __shfl_sync(FULL, winc, 31);
-        const bool smacc = nw <= static_cast<uint32_t>(HUB_ACC);
-        double* acc = smacc ? S.acc[warp] : ov;
+        // the running sums live in place in C (the row's range, L2-resident);
+        // a shared-memory copy for warps with few columns paid with 8 warps
+        // but not with 32 (numeric 51.7 -> 48.8 ms without it, R-MAT 18)
+        double* acc = ov;
         for (int64_t c0 = e0; c0 < e1; c0 += 32) {
             int64_t s, f;
             double av;
@@ -747,8 +744,6 @@ __global__ void __launch_bounds__(32 * NUM_NW) k_hub_num(const int32_t* __restri
                 __syncwarp();
             }
         }
-        if (smacc)
-            for (uint32_t x = lane; x < nw; x += 32) ov[x] = acc[x];
         __syncthreads();
     }
 }
@@ -1395,8 +1390,7 @@ struct HostProf {
 // after k_tile (hub_numeric). drows receives the BIG rows in ascending order.
 constexpr int64_t HUB_MAX_COLS = HUB_W;
 // CTAs per SM: the symbolic pass as many as fit (4 of 512 threads); the
-// numeric pass one (its shared memory; with 8 warps a second CTA was slower
-// too, R-MAT 18: 65.0 ms against 69.7 — the rows' running sums stay in L2)
+// numeric pass one of 1024 threads (58 registers: a second does not fit)
 int hub_grid(spg_ctx* ctx, bool numeric) {
     static const char* g = std::getenv("SPG_HUB_CTAS");
     return ctx->num_sms * (g ? std::atoi(g) : (numeric ? 1 : 2048 / (32 * SYM_NW)));
